@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Benchmark of the deterministic ScatterShuffle hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload hot|c1|c2|c3|c5]
+    python bench.py --impl reference ...     # the CPU oracle on a bounded sample
+
+One step = one whole shuffle (every scatter level in HBM and in shared memory
+plus the Fisher-Yates leaves) of the workload, resident in HBM, re-shuffling
+the previous step's output in place (same cost).  Rank 0 prints
+one JSON line.  Under torchrun (N > 1) every rank shuffles its own independent
+problem (seed + rank) -- replicas only, weak scaling -- and the
+time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "elements shuffled/s and effective HBM GB/s vs 8 TB/s peak, n=2^30 u32"
+SPEC_HBM_GBPS = 8000.0
+DTYPE = {4: "u32", 8: "u64", 16: "16B-record"}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """Polls NVML (SM clock + clock-event reasons) every ~5 ms on a thread."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz, self.ok = [], 0, None, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def workload_bytes(w, stats):
+    """Q11 effective bytes: 2*eb*(sum_l n_l + n_leafpass) with n_l every element
+    scattered at level l (HBM or shared memory) and the leaf pass over n."""
+    scattered = sum(stats["scattered_hbm"]) + sum(stats["scattered_smem"])
+    return 2 * w.elem_bytes * (scattered + w.n), scattered
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU oracle as it stands, bounded sample per step."""
+    if rank != 0:
+        return
+    import oracle
+    w = synth.WORKLOADS[args.workload]
+    n_s = args.ref_sample
+    a = synth.make_input_np(w, n=n_s)
+    for _ in range(args.warmup):
+        oracle.shuffle(a, w.k, w.L, w.seed)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.shuffle(a, w.k, w.L, w.seed)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    v = n_s / dt
+    sample = f"{n_s} of the workload's elements ({w.note}, k={w.k}, L={w.L}, seed={w.seed}), one shuffle per step"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE[w.elem_bytes], "data": "synthetic",
+            "config": {"workload": args.workload, "n": w.n, "elem_bytes": w.elem_bytes, "k": w.k, "L": w.L,
+                       "seed": w.seed},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(w, n_s):
+    import oracle
+    a = synth.make_input_np(w, n=n_s)
+    t0 = time.perf_counter()
+    oracle.shuffle(a, w.k, w.L, w.seed)
+    dt = time.perf_counter() - t0
+    return {"value": n_s / dt, "unit": "elements/s", "cores": 1, "kind": "oracle",
+            "sample": f"one oracle shuffle of the first {n_s} elements of the workload "
+                      f"({w.note}, k={w.k}, L={w.L}, seed={w.seed}); {dt:.1f} s on 1 host core"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="hot", choices=["hot", "c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 25)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import paper_2302_03317_b200 as shuf
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    w = synth.WORKLOADS[args.workload]
+    seed = w.seed + rank
+    if w.kind == "segmented":
+        lens = synth.c5_lengths(w.num_segments, w.seed)
+        off_np = synth.segment_offsets(lens)
+        n = int(off_np[-1])
+        w = synth.Workload(w.name, n, w.elem_bytes, w.k, w.L, w.seed, w.kind, w.num_segments, w.note)
+        d_off = torch.from_numpy(off_np.view(np.int64)).to(dev)
+        x = synth.make_input_torch(w, dev, offsets=off_np)
+    else:
+        d_off = None
+        x = synth.make_input_torch(w, dev)
+    plan = shuf.shuf_plan(w.n, w.elem_bytes, w.k, w.L, seed)
+    scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if d_off is None:
+            shuf.shuf_run(plan, x, scratch, stream)
+        else:
+            shuf.shuf_segmented(plan, x, d_off, scratch, stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    err = shuf.shuf_last_device_error(plan, stream)
+    if err:
+        raise SystemExit(f"device error {err}")
+    stats = shuf.shuf_last_run_stats(plan, stream)
+    launches_per_step = shuf.shuf_last_launch_count(plan)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- timed region: K steps, inputs (4 GiB for hot) >> L2, CUDA events on the launching stream
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms = ms_total / args.steps
+    value = w.n * world / (ms / 1e3)
+    eff_bytes, scattered = workload_bytes(w, stats)
+    eff_gbps = eff_bytes / (ms / 1e3) / 1e9
+
+    # ---- per-kernel breakdown (separate pass; every launch bracketed by events on `stream`)
+    prof = shuf.shuf_profile_run(plan, x, scratch, d_off, stream)
+    peaks, peak_src = load_peaks()
+    hbm_peak = float(peaks["hbm_gbs"])
+    eb = w.elem_bytes
+    kbytes = {"scatter": 2 * eb * sum(stats["scattered_hbm"]), "finish": 2 * eb * stats["finished"]}
+    kernels = {}
+    for name, (kms, cnt) in prof.items():
+        d = {"ms": round(kms, 4), "launches": cnt}
+        if name in kbytes and kms > 0:
+            d["algorithmic_bytes"] = kbytes[name]
+            d["GBps"] = round(kbytes[name] / (kms / 1e3) / 1e9, 1)
+        kernels[name] = d
+    dom = max(("scatter", "finish"), key=lambda c: prof[c][0])
+    dms, dcnt = prof[dom]
+    achieved = kbytes[dom] / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.workload, {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                "algorithmic_bytes_per_launch": kbytes[dom] / max(1, dcnt),
+                "avg_launch_ms": dms / max(1, dcnt)}
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies timed
+    e2e = None
+    if args.e2e_steps > 0:
+        host_in = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        host_in.copy_(x)
+        host_out = torch.empty_like(host_in, pin_memory=True)
+        nbytes = x.numel() * x.element_size()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            x.copy_(host_in, non_blocking=True)
+            step()
+            host_out.copy_(x, non_blocking=True)
+        f1.record(stream)
+        barrier()
+        e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": w.n * world / (e2e_ms / 1e3), "unit": "elements/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+        del host_in, host_out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w if w.kind != "segmented" else synth.WORKLOADS["c1"], min(args.cpu_sample, w.n))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": DTYPE[w.elem_bytes], "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {w.note}, k={w.k}, L={w.L}, seed={w.seed}", "n": w.n,
+                       "elem_bytes": w.elem_bytes, "k": w.k, "L": w.L, "seed": w.seed,
+                       "l2": "inputs larger than L2 (no flush)" if w.n * w.elem_bytes > (256 << 20)
+                       else "input fits in L2: not an HBM figure",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "eff_GBps": eff_gbps, "frac_of_8TBps": eff_gbps / SPEC_HBM_GBPS,
+            "frac_of_measured_copy": eff_gbps / hbm_peak, "effective_bytes_per_step": eff_bytes,
+            "elements_scattered_per_step": scattered, "levels": {"hbm": stats["scattered_hbm"],
+                                                                 "smem": stats["scattered_smem"]},
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * include/shuf.h -- C ABI of libshuf.so, the B200 (sm_100a) deterministic
+ * ScatterShuffle hot path.
+ *
+ * What it computes (PAPER.md = arXiv 2302.03317 text):
+ *   A uniformly random permutation of an array of n elements by recursive
+ *   ScatterShuffle: every element of a segment draws a uniform
+ *   bucket id in [0,k), the segment is grouped by bucket with a
+ *   STABLE permutation ("some permutation pi that sorts A"),
+ *   recursion continues on every bucket longer than L, and buckets of at most
+ *   L elements ("leaves") are finished by Fisher-Yates exactly as Fig. 1
+ *   (P:107-110).  Every draw is a counter-based Philox4x32-10 draw mapped to
+ *   [0,s) by Lemire's method -- DESIGN.md D1-D5 -- so the result is
+ *   a pure function of (n, k, L, seed) and equals the CPU oracle bit for bit.
+ *
+ * Conventions for every entry point:
+ *   - Device pointers are CUDA device addresses (e.g. torch .data_ptr()),
+ *     16-byte aligned; host pointers are plain host memory.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *     All device work is enqueued on it; no call synchronises the stream
+ *     unless its comment says so.  No call allocates device memory except
+ *     shuf_plan (a few hundred bytes of plan metadata).
+ *   - The caller owns ptr, scratch, offsets and the stream.  The plan owns
+ *     only its own metadata.  A plan may be used by one stream at a time.
+ *   - Errors: argument errors are returned synchronously and nothing is
+ *     enqueued.  CUDA launch errors return SHUF_ERR_CUDA.  Errors detected on
+ *     the device (depth bound exceeded, scratch too small) are latched in the
+ *     plan's device status word and read by shuf_last_device_error() (which
+ *     synchronises).  There is no CPU fallback: without a CUDA device every
+ *     compute entry point returns SHUF_ERR_CUDA.
+ */
+#ifndef SHUF_H
+#define SHUF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct shuf_plan_s *shuf_plan_t;
+
+typedef enum {
+    SHUF_OK = 0,
+    SHUF_ERR_INVALID_ARG = 1, /* n/k/L/elem_bytes/offsets outside the domain     */
+    SHUF_ERR_UNSUPPORTED = 2, /* valid for the oracle, not supported on device   */
+    SHUF_ERR_ALIGNMENT = 3,   /* ptr/scratch/offsets not 16-byte aligned         */
+    SHUF_ERR_SCRATCH = 4,     /* scratch_bytes smaller than shuf_scratch_bytes() */
+    SHUF_ERR_DEPTH = 5,       /* more levels than planned (device-detected)      */
+    SHUF_ERR_CUDA = 6         /* a CUDA runtime error; see shuf_last_cuda_error  */
+} shuf_status;
+
+/* Create a plan for shuffling n elements of elem_bytes bytes each with k
+ * buckets per scatter level, leaves of at most L elements, and seed `seed`
+ * (D2: the single-problem key is K = seed).
+ * Domain: elem_bytes in {4, 8, 16}; 2 <= k <= 4096 (any k; powers of two take
+ * the shift path of P:99); 1 <= L <= the device leaf capacity (L*elem_bytes
+ * <= 96 KiB).  n may be 0 or 1 (no-ops).  For shuf_segmented, n is the total
+ * number of elements over all segments.
+ * Returns NULL on error; the reason is in shuf_last_status(). */
+shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, uint32_t L, uint64_t seed);
+
+/* Status of the last shuf_plan call on this thread. */
+shuf_status shuf_last_status(void);
+
+/* Bytes of device scratch shuf_run / shuf_segmented need for this plan:
+ * one ping-pong buffer of n*elem_bytes plus O(k * n / chunk + n / S_fuse)
+ * words of per-level metadata.  Writes *bytes. */
+shuf_status shuf_scratch_bytes(shuf_plan_t p, uint64_t *bytes);
+
+/* Shuffle ptr[0..n) in place (result in ptr) using `scratch` (device, at
+ * least shuf_scratch_bytes).  Stream-ordered, no host synchronisation, no
+ * allocation.  The permutation is DESIGN.md D6 with K = seed. */
+shuf_status shuf_run(shuf_plan_t p, void *ptr, void *scratch, uint64_t scratch_bytes, void *stream);
+
+/* Segmented batch shuffle (D7): segment s = ptr[off[s] .. off[s+1])
+ * is shuffled independently with key K(seed, s) = seed + s*0x9E3779B97F4A7C15
+ * and segment-relative positions.  d_offsets: DEVICE array of num_segments+1
+ * ascending uint64, d_offsets[0] = 0, d_offsets[num_segments] = n (the plan's
+ * n); empty segments allowed.  The offsets are not validated on the device
+ * beyond the plan's bounds. */
+shuf_status shuf_segmented(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, uint64_t num_segments,
+                           void *scratch, uint64_t scratch_bytes, void *stream);
+
+/* Test hook: like shuf_run, but only scatter levels l < max_levels run (in
+ * HBM or in shared memory alike) and leaves are Fisher-Yates'd only if
+ * run_leaves != 0; the state reached is left in ptr.  Equals the oracle's
+ * level-limited mode (oracle_shuffle(..., max_levels, run_leaves)). */
+shuf_status shuf_debug_run_levels(shuf_plan_t p, void *ptr, void *scratch, uint64_t scratch_bytes, void *stream,
+                                  uint32_t max_levels, int run_leaves);
+
+/* Test hook (raw-draw parity): out[i] = D4 bucket draw at (level, p0 + i)
+ * under key K for bucket count k; d_out is a device array of count uint32. */
+shuf_status shuf_debug_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count, uint32_t k,
+                                    uint32_t *d_out, void *stream);
+
+/* Test hook: out[i] = D5 Fisher-Yates draw at position d_P[i] with bound
+ * d_s[i] (>= 1) under key K; device arrays of count elements. */
+shuf_status shuf_debug_fy_draws(uint64_t K, const uint64_t *d_P, const uint32_t *d_s, uint64_t count,
+                                uint32_t *d_out, void *stream);
+
+/* Kernel classes reported by shuf_profile_run. */
+enum {
+    SHUF_K_INIT = 0,    /* work-list initialisation                         */
+    SHUF_K_HIST = 1,    /* per-chunk bucket histogram (draws only, no data)  */
+    SHUF_K_SCAN = 2,    /* decoupled-lookback exclusive scan of the counts   */
+    SHUF_K_PLAN = 3,    /* next-level segment planner                        */
+    SHUF_K_SCATTER = 4, /* HBM stable scatter                                */
+    SHUF_K_FINISH = 5,  /* fused shared-memory finish (levels + FY leaves)   */
+    SHUF_K_CLASSES = 6
+};
+
+/* Measurement hook: enqueue the same work as shuf_run (d_offsets == NULL) or
+ * shuf_segmented, bracket every kernel launch with CUDA events on `stream`,
+ * SYNCHRONISE the stream, and write per-class summed milliseconds and launch
+ * counts to host arrays of SHUF_K_CLASSES entries.  Allocates events. */
+shuf_status shuf_profile_run(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, uint64_t num_segments,
+                             void *scratch, uint64_t scratch_bytes, void *stream, float *ms_by_class,
+                             uint32_t *launches_by_class);
+
+/* Measurement counters of the last run on this plan (synchronises):
+ * out[0] = elements written by the fused finish, out[1] = elements in
+ * Fisher-Yates leaves, out[2+2l] = elements scattered through HBM at level l,
+ * out[3+2l] = elements scattered in shared memory at level l (l < 256).
+ * Writes min(count, 514) entries; the rest are zero. */
+shuf_status shuf_last_run_stats(shuf_plan_t p, void *stream, uint64_t *out, uint32_t count);
+
+/* Synchronise `stream` and return the plan's latched device error (SHUF_OK
+ * if none), clearing it. */
+shuf_status shuf_last_device_error(shuf_plan_t p, void *stream);
+
+/* The cudaError_t behind the last SHUF_ERR_CUDA returned for this plan. */
+int shuf_last_cuda_error(shuf_plan_t p);
+
+/* Number of kernel launches the last shuf_run/shuf_segmented enqueued. */
+uint64_t shuf_last_launch_count(shuf_plan_t p);
+
+/* Planned number of HBM (global) scatter levels for this plan. */
+uint32_t shuf_planned_levels(shuf_plan_t p);
+
+void shuf_destroy(shuf_plan_t p);
+const char *shuf_status_string(shuf_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHUF_H */

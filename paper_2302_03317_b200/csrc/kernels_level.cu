@@ -1,0 +1,483 @@
+// HBM-resident ("global") scatter level: init, histogram, decoupled-lookback
+// scan, segment planner and the TMA-staged stable scatter.
+//
+// One level l over the active segments computes, for every segment s of
+// length m at [a, a+m) (D6, P:140-142 with pi stable):
+//   c_b = #{i : bucket(l, i) = b},  o_b = a + sum_{b'<b} c_b',
+//   OUT[o_b++] = IN[i] for ascending i.
+// Segments are cut into chunks of C elements; a CTA owns a chunk and walks
+// it tile by tile in order, so the destination of (segment, bucket, chunk)
+// is the exclusive prefix of the counts flattened in (segment, bucket,
+// chunk) order (k_scan), and within a chunk a per-bucket running offset plus
+// the stable in-tile rank gives every element's destination.
+#include <cuda_runtime.h>
+
+#include "block_ops.cuh"
+#include "shuf_internal.cuh"
+
+namespace shuf {
+
+__device__ __forceinline__ void latch_error(Header* h, uint32_t code) { atomicCAS(&h->error, 0u, code); }
+
+__device__ __forceinline__ uint64_t gtid() { return (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ uint64_t gstride() { return (uint64_t)gridDim.x * blockDim.x; }
+
+// ------------------------------------------------------------------ init --
+__global__ void k_init_single(RunParams rp, LevelParams lp0) {
+    const uint64_t n = rp.n;
+    if (gtid() == 0) {
+        rp.hdr->root_off[0] = 0;
+        rp.hdr->root_off[1] = n;
+    }
+    if (!(n > rp.S_fuse && rp.max_levels > 0)) return;
+    const uint64_t nch = (n + rp.chunk - 1) / rp.chunk;
+    if (gtid() == 0) {
+        SegDesc sd;
+        sd.start = 0;
+        sd.len = n;
+        sd.origin = 0;
+        sd.key = rp.seed;  // K(seed, 0) = seed (D2)
+        sd.cbase = 0;
+        sd.nchunks = (uint32_t)nch;
+        sd.pad = 0;
+        lp0.segs[0] = sd;
+        lp0.ctr->nseg = 1;
+        lp0.ctr->nchunk = (uint32_t)nch;
+    }
+    for (uint64_t j = gtid(); j < nch; j += gstride()) lp0.chunks[j] = ChunkDesc{0u, (uint32_t)j};
+}
+
+__global__ void k_init_segmented(RunParams rp, LevelParams lp0, const uint64_t* __restrict__ off, uint64_t nsegs) {
+    if (gtid() == 0 && (off[0] != 0 || off[nsegs] != rp.n)) latch_error(rp.hdr, 1u /*SHUF_ERR_INVALID_ARG*/);
+    for (uint64_t s = gtid(); s < nsegs; s += gstride()) {
+        const uint64_t a = off[s], b = off[s + 1];
+        if (b < a) {
+            latch_error(rp.hdr, 1u);
+            continue;
+        }
+        const uint64_t len = b - a;
+        if (!(len > rp.S_fuse && rp.max_levels > 0)) continue;
+        const uint64_t nch = (len + rp.chunk - 1) / rp.chunk;
+        const uint32_t si = atomicAdd(&lp0.ctr->nseg, 1u);
+        const uint32_t cb = atomicAdd(&lp0.ctr->nchunk, (uint32_t)nch);
+        if (si >= lp0.max_segs || cb + nch > lp0.max_chunks) {
+            latch_error(rp.hdr, 4u /*SHUF_ERR_SCRATCH*/);
+            continue;
+        }
+        SegDesc sd;
+        sd.start = a;
+        sd.len = len;
+        sd.origin = a;
+        sd.key = rp.seed + s * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
+        sd.cbase = (uint64_t)cb * rp.k;
+        sd.nchunks = (uint32_t)nch;
+        sd.pad = 0;
+        lp0.segs[si] = sd;
+        for (uint64_t c = 0; c < nch; ++c) lp0.chunks[cb + c] = ChunkDesc{si, (uint32_t)c};
+    }
+}
+
+// ------------------------------------------------------------- histogram --
+// counts[cbase + b*nchunks + c] = #{p in chunk c : bucket(l, p) = b}.
+// Regenerates the draws from Philox counters; reads no element data.
+__global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp) {
+    extern __shared__ uint32_t hist[];
+    const uint32_t nchunk = lp.ctr->nchunk;
+    const uint64_t E = (uint64_t)nchunk * rp.k;
+    const uint64_t ntiles = (E + kScanTile - 1) / kScanTile;
+    for (uint64_t t = gtid(); t < ntiles; t += gstride()) lp.status[t] = 0;
+    if (gtid() == 0) {
+        lp.ctr->scan_ticket = 0;
+        lp.nctr->nseg = 0;
+        lp.nctr->nchunk = 0;
+    }
+    const uint32_t k = rp.k;
+    for (uint32_t j = blockIdx.x; j < nchunk; j += gridDim.x) {
+        for (uint32_t b = threadIdx.x; b < k; b += kThreads) hist[b] = 0;
+        __syncthreads();
+        const ChunkDesc ch = lp.chunks[j];
+        const SegDesc sg = lp.segs[ch.seg];
+        const uint64_t q0 = sg.start + (uint64_t)ch.c * rp.chunk;
+        const uint64_t q1 = min(sg.start + sg.len, q0 + rp.chunk);
+        const uint64_t P0 = q0 - sg.origin, m = q1 - q0;
+        const PhiloxKey key = make_key(sg.key);
+        const uint64_t g0 = P0 >> 3, ng = ((P0 + m - 1) >> 3) - g0 + 1;
+        for (uint64_t t = threadIdx.x; t < ng; t += kThreads) {
+            const uint64_t g = g0 + t;
+            const uint4 w = bucket_group_words(key, lp.level, g);
+            const uint64_t pb = g << 3;
+#pragma unroll
+            for (uint32_t jj = 0; jj < 8; ++jj) {
+                const uint64_t p = pb + jj;
+                if (p >= P0 && p < P0 + m) {
+                    const uint32_t b = bucket_from_lane(lane16(w, jj), key, lp.level, p, rp.bp);
+                    atomicAdd(&hist[b], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < k; b += kThreads)
+            lp.counts[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] = hist[b];
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ scan --
+// Single-pass exclusive scan (decoupled lookback, Merrill & Garland) of the
+// u32 counts into u64 prefixes.  Tiles are claimed in order through a ticket
+// so every predecessor of a claimed tile is owned by a running CTA.
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t warp_inclusive_sum64(uint64_t v) {
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= (uint32_t)o) v += t;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) k_scan(RunParams rp, LevelParams lp) {
+    __shared__ uint64_t wsum[kWarps + 1];
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_excl;
+    constexpr uint32_t PER = kScanTile / kThreads;  // 8
+    const uint64_t E = (uint64_t)lp.ctr->nchunk * rp.k;
+    const uint64_t ntiles = (E + kScanTile - 1) / kScanTile;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    for (;;) {
+        if (tid == 0) s_tile = atomicAdd(&lp.ctr->scan_ticket, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)tid * PER;
+        uint32_t v[PER];
+        uint64_t s = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < PER; ++i) {
+            v[i] = (base + i < E) ? lp.counts[base + i] : 0u;
+            s += v[i];
+        }
+        const uint64_t incl = warp_inclusive_sum64(s);
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            uint64_t x = lane < (uint32_t)kWarps ? wsum[lane] : 0ull;
+            uint64_t xi = warp_inclusive_sum64(x);
+            if (lane < (uint32_t)kWarps) wsum[lane] = xi - x;
+            if (lane == kWarps - 1) wsum[kWarps] = xi;
+        }
+        __syncthreads();
+        const uint64_t agg = wsum[kWarps];
+        if (warp == 0) {
+            uint64_t excl = 0;
+            if (tile == 0) {
+                if (lane == 0) st_release_u64(&lp.status[0], kFlagInc | agg);
+            } else {
+                if (lane == 0) st_release_u64(&lp.status[tile], kFlagAgg | agg);
+                int64_t j = (int64_t)tile - 1;
+                for (;;) {
+                    const int64_t idx = j - (int64_t)lane;
+                    uint64_t st = kFlagInc;  // before tile 0: inclusive zero
+                    if (idx >= 0) {
+                        do {
+                            st = ld_acquire_u64(&lp.status[idx]);
+                        } while ((st >> 62) == 0);
+                    }
+                    const uint32_t incmask = __ballot_sync(0xFFFFFFFFu, (st >> 62) == 2);
+                    uint64_t val = st & kValMask;
+                    if (incmask) {
+                        const uint32_t p = __ffs(incmask) - 1;
+                        if (lane > p) val = 0;
+                    }
+                    // reduce over the warp
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, o);
+                    excl += val;
+                    if (incmask) break;
+                    j -= 32;
+                }
+                if (lane == 0) st_release_u64(&lp.status[tile], kFlagInc | (excl + agg));
+            }
+            if (lane == 0) s_excl = excl;
+        }
+        __syncthreads();
+        uint64_t run = s_excl + wsum[warp] + incl - s;
+#pragma unroll
+        for (uint32_t i = 0; i < PER; ++i) {
+            if (base + i < E) lp.prefix[base + i] = run;
+            run += v[i];
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------- planner --
+// Child b of segment s: [start_s + P(s,b,0) - P(s,0,0), next).
+// Children longer than S_fuse become segments of level l+1 (chunked);
+// shorter ones are finished in shared memory by k_finish_children.
+__device__ __forceinline__ void child_range(const SegDesc& sg, const uint64_t* __restrict__ prefix, uint32_t k,
+                                            uint32_t b, uint64_t& start, uint64_t& len) {
+    const uint64_t base0 = prefix[sg.cbase];
+    const uint64_t s0 = prefix[sg.cbase + (uint64_t)b * sg.nchunks] - base0;
+    const uint64_t s1 = (b + 1 < k) ? prefix[sg.cbase + (uint64_t)(b + 1) * sg.nchunks] - base0 : sg.len;
+    start = sg.start + s0;
+    len = s1 - s0;
+}
+
+__global__ void k_plan(RunParams rp, LevelParams lp) {
+    const uint64_t nchild = (uint64_t)lp.ctr->nseg * rp.k;
+    const uint32_t next = lp.level + 1;
+    for (uint64_t i = gtid(); i < nchild; i += gstride()) {
+        const uint32_t s = (uint32_t)(i / rp.k), b = (uint32_t)(i % rp.k);
+        const SegDesc sg = lp.segs[s];
+        uint64_t start, len;
+        child_range(sg, lp.prefix, rp.k, b, start, len);
+        if (len <= rp.S_fuse) continue;  // finished by k_finish_children
+        if (next >= rp.max_levels) continue;  // debug level limit: copied out by k_finish_children
+        if (next >= rp.planned_levels) {
+            latch_error(rp.hdr, 5u /*SHUF_ERR_DEPTH*/);
+            continue;
+        }
+        const uint64_t nch = (len + rp.chunk - 1) / rp.chunk;
+        const uint32_t si = atomicAdd(&lp.nctr->nseg, 1u);
+        const uint32_t cb = atomicAdd(&lp.nctr->nchunk, (uint32_t)nch);
+        if (si >= lp.max_segs || cb + nch > lp.max_chunks) {
+            latch_error(rp.hdr, 4u);
+            continue;
+        }
+        SegDesc nd;
+        nd.start = start;
+        nd.len = len;
+        nd.origin = sg.origin;
+        nd.key = sg.key;
+        nd.cbase = (uint64_t)cb * rp.k;
+        nd.nchunks = (uint32_t)nch;
+        nd.pad = 0;
+        lp.nsegs[si] = nd;
+        for (uint64_t c = 0; c < nch; ++c) lp.nchunks[cb + c] = ChunkDesc{si, (uint32_t)c};
+    }
+}
+
+// ---------------------------------------------------------------- scatter --
+template <int EB>
+struct ScatterSmem {
+    static constexpr uint32_t T = kTileBytes / EB;  // elements per tile
+    static constexpr uint32_t Q = T / kWarps;       // elements per warp
+    static constexpr uint32_t R = Q / 32;           // rounds per warp
+};
+
+template <int EB>
+__host__ __device__ inline uint32_t scatter_smem_layout(uint32_t k, uint32_t* o_in, uint32_t* o_stg, uint32_t* o_slotb,
+                                                        uint32_t* o_draws, uint32_t* o_cwb, uint32_t* o_run,
+                                                        uint32_t* o_bst, uint32_t* o_wsum, uint32_t* o_bar) {
+    constexpr uint32_t T = ScatterSmem<EB>::T;
+    uint32_t off = 0;
+    *o_in = off;
+    off += T * EB + 16;
+    *o_stg = off;
+    off += T * EB;
+    *o_run = off;
+    off += k * 8;
+    *o_bst = off;
+    off += (k + 1) * 4;
+    off = (off + 15) & ~15u;
+    *o_wsum = off;
+    off += (kWarps + 1) * 4;
+    off = (off + 15) & ~15u;
+    *o_bar = off;
+    off += 16;
+    *o_slotb = off;
+    off += T * 2;
+    *o_draws = off;
+    off += T * 2;
+    *o_cwb = off;
+    off += k * kWarps * 2;
+    return (off + 15) & ~15u;
+}
+
+template <int EB>
+__global__ void __launch_bounds__(kThreads, 2) k_scatter(RunParams rp, LevelParams lp) {
+    using E = typename ElemT<EB>::type;
+    constexpr uint32_t T = ScatterSmem<EB>::T, Q = ScatterSmem<EB>::Q, R = ScatterSmem<EB>::R;
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint32_t o_in, o_stg, o_slotb, o_draws, o_cwb, o_run, o_bst, o_wsum, o_bar;
+    const uint32_t k = rp.k;
+    scatter_smem_layout<EB>(k, &o_in, &o_stg, &o_slotb, &o_draws, &o_cwb, &o_run, &o_bst, &o_wsum, &o_bar);
+    unsigned char* tile_in = sm + o_in;
+    E* staging = reinterpret_cast<E*>(sm + o_stg);
+    uint16_t* slotb = reinterpret_cast<uint16_t*>(sm + o_slotb);
+    uint16_t* draws = reinterpret_cast<uint16_t*>(sm + o_draws);
+    uint16_t* cwb = reinterpret_cast<uint16_t*>(sm + o_cwb);  // [b][w]
+    uint64_t* running = reinterpret_cast<uint64_t*>(sm + o_run);
+    uint32_t* bst = reinterpret_cast<uint32_t*>(sm + o_bst);
+    uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + o_wsum);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + o_bar);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    const uint32_t nchunk = lp.ctr->nchunk;
+    const unsigned char* __restrict__ src = lp.src;
+    E* __restrict__ dst = reinterpret_cast<E*>(lp.dst);
+
+    for (uint32_t j = blockIdx.x; j < nchunk; j += gridDim.x) {
+        const ChunkDesc ch = lp.chunks[j];
+        const SegDesc sg = lp.segs[ch.seg];
+        const PhiloxKey key = make_key(sg.key);
+        const uint64_t c0 = sg.start + (uint64_t)ch.c * rp.chunk;
+        const uint64_t c1 = min(sg.start + sg.len, c0 + rp.chunk);
+        if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->scattered_hbm[lp.level], (unsigned long long)(c1 - c0));
+        {
+            const uint64_t base0 = lp.prefix[sg.cbase];
+            for (uint32_t b = tid; b < k; b += kThreads)
+                running[b] = sg.start + lp.prefix[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] - base0;
+        }
+        for (uint64_t q0 = c0; q0 < c1; q0 += T) {
+            const uint32_t cnt = (uint32_t)((c1 - q0) < (uint64_t)T ? (c1 - q0) : (uint64_t)T);
+            const uint64_t q1 = q0 + cnt;
+            // ---- 1. load the tile: aligned body by one bulk copy, head/tail by words
+            const uint64_t x0 = q0 * EB, x1 = q1 * EB;
+            const uint64_t fl = x0 & ~15ull;                // smem byte 0 <-> global byte fl
+            const uint64_t A = (x0 + 15) & ~15ull, B = x1 & ~15ull;
+            const bool body = B > A;
+            if (body && tid == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(bar, (uint32_t)(B - A));
+                bulk_g2s(tile_in + (A - fl), src + A, (uint32_t)(B - A), bar);
+            }
+            {
+                // head bytes [x0, min(A, x1)) and tail bytes [max(B, A), x1) as 4-byte words
+                const uint64_t hEnd = body ? A : x1;
+                const uint32_t nh = (uint32_t)((hEnd - x0) >> 2);
+                const uint64_t tBeg = body ? B : x1;
+                const uint32_t nt = (uint32_t)((x1 - tBeg) >> 2);
+                if (tid < nh)
+                    *reinterpret_cast<uint32_t*>(tile_in + (x0 - fl) + 4 * tid) =
+                        *reinterpret_cast<const uint32_t*>(src + x0 + 4 * tid);
+                else if (tid >= 32 && tid - 32 < nt)
+                    *reinterpret_cast<uint32_t*>(tile_in + (tBeg - fl) + 4 * (tid - 32)) =
+                        *reinterpret_cast<const uint32_t*>(src + tBeg + 4 * (tid - 32));
+            }
+            // ---- 2. draws (overlaps the bulk load), zero the per-warp counters
+            draws_to_smem(draws, q0 - sg.origin, cnt, key, lp.level, rp.bp);
+            for (uint32_t i = tid; i < k * kWarps; i += kThreads) cwb[i] = 0;
+            __syncthreads();
+            // ---- 3. stable rank: warp w owns [w*Q, (w+1)*Q), rounds of 32 in order
+            uint32_t rk[R];
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                const uint32_t e = warp * Q + r * 32 + lane;
+                const bool valid = e < cnt;
+                const uint32_t b = valid ? draws[e] : 0xFFFFu;
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
+                const uint32_t old = valid ? cwb[b * kWarps + warp] : 0u;
+                __syncwarp();
+                if (valid && lane == (uint32_t)(__ffs(peers) - 1)) cwb[b * kWarps + warp] = (uint16_t)(old + __popc(peers));
+                __syncwarp();
+                rk[r] = old + __popc(peers & lanemask_lt());
+            }
+            __syncthreads();
+            // ---- 4. exclusive scan over (bucket, warp): tile-local bases
+            block_exclusive_scan(cwb, k * kWarps, wsum);
+            for (uint32_t b = tid; b < k; b += kThreads) bst[b] = cwb[b * kWarps];
+            if (tid == 0) bst[k] = cnt;
+            if (body) mbar_wait(bar, phase);
+            __syncthreads();
+            if (body) phase ^= 1u;
+            // ---- 5. reorder into staging (bucket-major, stable)
+            const unsigned char* tin = tile_in + (x0 - fl);
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                const uint32_t e = warp * Q + r * 32 + lane;
+                if (e < cnt) {
+                    const uint32_t b = draws[e];
+                    const uint32_t slot = cwb[b * kWarps + warp] + rk[r];
+                    staging[slot] = *reinterpret_cast<const E*>(tin + (size_t)e * EB);
+                    slotb[slot] = (uint16_t)b;
+                }
+            }
+            __syncthreads();
+            // ---- 6. write the bucket runs
+            for (uint32_t s = tid; s < cnt; s += kThreads) {
+                const uint32_t b = slotb[s];
+                dst[running[b] + (s - bst[b])] = staging[s];
+            }
+            __syncthreads();
+            for (uint32_t b = tid; b < k; b += kThreads) running[b] += bst[b + 1] - bst[b];
+            __syncthreads();
+        }
+    }
+}
+
+// --------------------------------------------------------------- launchers --
+cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid) {
+    k_init_single<<<grid, 256, 0, s>>>(rp, lp0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_segmented(const RunParams& rp, const LevelParams& lp0, const uint64_t* d_offsets,
+                                  uint64_t num_segments, cudaStream_t s, int grid) {
+    k_init_segmented<<<grid, 256, 0, s>>>(rp, lp0, d_offsets, num_segments);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hist(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    k_hist<<<grid, kThreads, rp.k * sizeof(uint32_t), s>>>(rp, lp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    k_scan<<<grid, kThreads, 0, s>>>(rp, lp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    k_plan<<<grid, 256, 0, s>>>(rp, lp);
+    return cudaGetLastError();
+}
+
+uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k) {
+    uint32_t a, b, c, d, e, f, g, h, i;
+    switch (eb) {
+    case 4: return scatter_smem_layout<4>(k, &a, &b, &c, &d, &e, &f, &g, &h, &i);
+    case 8: return scatter_smem_layout<8>(k, &a, &b, &c, &d, &e, &f, &g, &h, &i);
+    default: return scatter_smem_layout<16>(k, &a, &b, &c, &d, &e, &f, &g, &h, &i);
+    }
+}
+
+cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    const uint32_t smem = scatter_smem_bytes(rp.eb, rp.k);
+    switch (rp.eb) {
+    case 4: k_scatter<4><<<grid, kThreads, smem, s>>>(rp, lp); break;
+    case 8: k_scatter<8><<<grid, kThreads, smem, s>>>(rp, lp); break;
+    default: k_scatter<16><<<grid, kThreads, smem, s>>>(rp, lp); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t configure_scatter(uint32_t smem) {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_scatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_scatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+    return cudaFuncSetAttribute(k_scatter<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+cudaError_t occupancy_level(uint32_t eb, uint32_t k, int* hist, int* scan, int* scatter) {
+    cudaError_t e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(hist, k_hist, kThreads, k * sizeof(uint32_t)))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(scan, k_scan, kThreads, 0))) return e;
+    const uint32_t smem = scatter_smem_bytes(eb, k);
+    switch (eb) {
+    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(scatter, k_scatter<4>, kThreads, smem);
+    case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(scatter, k_scatter<8>, kThreads, smem);
+    default: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(scatter, k_scatter<16>, kThreads, smem);
+    }
+}
+
+}  // namespace shuf

@@ -1,0 +1,403 @@
+// C ABI of libshuf.so (include/shuf.h): plan, scratch layout, stream-ordered
+// level loop.  No host synchronisation and no allocation inside shuf_run /
+// shuf_segmented: every level's work list lives on the device and each
+// kernel is a persistent grid that reads its own work count.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/shuf.h"
+#include "philox.cuh"
+#include "shuf_internal.cuh"
+
+using namespace shuf;
+
+struct shuf_plan_s {
+    uint64_t n;
+    uint32_t eb, k, L;
+    uint64_t seed;
+    uint32_t S_fuse, chunk, levels;
+    ScratchLayout lay;
+    // device setup (lazily, first run)
+    bool dev_ready;
+    int sms;
+    int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small;
+    uint32_t finish_smem, scatter_smem;
+    int last_cuda_error;
+    uint64_t last_launches;
+    Header* last_hdr;
+};
+
+static thread_local shuf_status g_last_status = SHUF_OK;
+
+static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// Largest S with finish_smem_bytes(S) <= the opt-in shared-memory limit,
+// capped so that in-smem frontiers (<= S/(L+1) entries) fit kFrontierCap and
+// u16 indices suffice.
+static uint32_t pick_s_fuse(uint32_t eb, uint32_t k, uint32_t L) {
+    uint32_t lo = 1, hi = 65535;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi + 1) / 2;
+        if (finish_smem_bytes(mid, eb, k) <= kSmemLimit) lo = mid;
+        else hi = mid - 1;
+    }
+    uint64_t cap = (uint64_t)kFrontierCap * ((uint64_t)L + 1);
+    if (cap < lo) lo = (uint32_t)cap;
+    return lo;
+}
+
+// Global levels needed until the largest segment fits S_fuse, with a
+// 12-sigma binomial margin per level, plus one spare level.
+static uint32_t plan_levels(uint64_t n, uint32_t k, uint32_t S_fuse) {
+    if (n <= S_fuse) return 0;
+    double m = (double)n;
+    uint32_t g = 0;
+    while (m > S_fuse && g < kMaxLevels) {
+        ++g;
+        double mu = m / k;
+        m = mu + 12.0 * std::sqrt(mu) + 32.0;
+        if (m >= (double)n) m = (double)n;  // k small: still shrinks in expectation
+        if (g > 200) break;
+    }
+    return g + 1 > kMaxLevels ? kMaxLevels : g + 1;
+}
+
+static void compute_layout(shuf_plan_s* p) {
+    ScratchLayout& l = p->lay;
+    const uint64_t n = p->n;
+    l.max_segs = n / ((uint64_t)p->S_fuse + 1) + 1;
+    l.max_chunks = n / p->chunk + l.max_segs + 1;
+    l.max_entries = l.max_chunks * p->k;
+    l.max_tiles = (l.max_entries + kScanTile - 1) / kScanTile + 1;
+    uint64_t off = 0;
+    l.pingpong = off;
+    off = align_up(off + n * p->eb + 16, 256);
+    l.header = off;
+    off = align_up(off + sizeof(Header), 256);
+    for (int s = 0; s < 2; ++s) {
+        l.segs[s] = off;
+        off = align_up(off + l.max_segs * sizeof(SegDesc), 256);
+        l.chunks[s] = off;
+        off = align_up(off + l.max_chunks * sizeof(ChunkDesc), 256);
+        l.counts[s] = off;
+        off = align_up(off + l.max_entries * 4, 256);
+        l.prefix[s] = off;
+        off = align_up(off + l.max_entries * 8, 256);
+        l.status[s] = off;
+        off = align_up(off + l.max_tiles * 8, 256);
+    }
+    l.total = off;
+}
+
+extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, uint32_t L, uint64_t seed) {
+    g_last_status = SHUF_OK;
+    if (!(elem_bytes == 4 || elem_bytes == 8 || elem_bytes == 16) && elem_bytes != 0) {
+        g_last_status = SHUF_ERR_UNSUPPORTED;
+        return nullptr;
+    }
+    if (elem_bytes == 0 || k < 2 || k > 65536 || L < 1) {
+        g_last_status = SHUF_ERR_INVALID_ARG;
+        return nullptr;
+    }
+    if (k > kMaxK) {
+        g_last_status = SHUF_ERR_UNSUPPORTED;
+        return nullptr;
+    }
+    const uint32_t S = pick_s_fuse(elem_bytes, k, L);
+    if (L > S) {
+        g_last_status = SHUF_ERR_UNSUPPORTED;
+        return nullptr;
+    }
+    shuf_plan_s* p = new (std::nothrow) shuf_plan_s();
+    if (!p) {
+        g_last_status = SHUF_ERR_INVALID_ARG;
+        return nullptr;
+    }
+    p->n = n;
+    p->eb = elem_bytes;
+    p->k = k;
+    p->L = L;
+    p->seed = seed;
+    p->S_fuse = S;
+    const uint32_t T = kTileBytes / elem_bytes;
+    uint64_t C = (n + 16383) / 16384;
+    C = align_up(C < T ? T : C, T);
+    if (C > 0x40000000ull) C = 0x40000000ull;
+    p->chunk = (uint32_t)C;
+    p->levels = plan_levels(n, k, S);
+    compute_layout(p);
+    return p;
+}
+
+extern "C" shuf_status shuf_last_status(void) { return g_last_status; }
+
+extern "C" shuf_status shuf_scratch_bytes(shuf_plan_t p, uint64_t* bytes) {
+    if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    *bytes = p->lay.total;
+    return SHUF_OK;
+}
+
+extern "C" uint32_t shuf_planned_levels(shuf_plan_t p) { return p ? p->levels : 0; }
+extern "C" int shuf_last_cuda_error(shuf_plan_t p) { return p ? p->last_cuda_error : 0; }
+extern "C" uint64_t shuf_last_launch_count(shuf_plan_t p) { return p ? p->last_launches : 0; }
+
+static shuf_status cuda_fail(shuf_plan_s* p, cudaError_t e) {
+    if (p) p->last_cuda_error = (int)e;
+    return SHUF_ERR_CUDA;
+}
+
+static cudaError_t device_setup(shuf_plan_s* p) {
+    if (p->dev_ready) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e) return e;
+    if ((e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    p->finish_smem = finish_smem_bytes(p->S_fuse, p->eb, p->k);
+    p->scatter_smem = scatter_smem_bytes(p->eb, p->k);
+    if ((e = configure_finish(p->finish_smem))) return e;
+    if ((e = configure_scatter(p->scatter_smem))) return e;
+    // persistent grids: SM count x resident CTAs per SM
+    int oh = 1, os = 1, osc = 1, of = 1;
+    if ((e = occupancy_level(p->eb, p->k, &oh, &os, &osc))) return e;
+    if ((e = occupancy_finish(p->eb, p->finish_smem, &of))) return e;
+    auto clamp1 = [](int v) { return v < 1 ? 1 : v; };
+    p->grid_hist = p->sms * clamp1(oh);
+    p->grid_scan = p->sms * clamp1(os);
+    p->grid_scatter = p->sms * clamp1(osc);
+    p->grid_finish = p->sms * clamp1(of);
+    p->grid_small = p->sms * 4;
+    p->dev_ready = true;
+    return cudaSuccess;
+}
+
+static LevelParams level_params(const shuf_plan_s* p, unsigned char* sc, unsigned char* buf0, uint32_t level) {
+    const ScratchLayout& l = p->lay;
+    Header* hdr = reinterpret_cast<Header*>(sc + l.header);
+    const int s = (int)(level & 1u), t = s ^ 1;
+    LevelParams lp;
+    lp.level = level;
+    lp.slot = s;
+    lp.segs = reinterpret_cast<SegDesc*>(sc + l.segs[s]);
+    lp.chunks = reinterpret_cast<ChunkDesc*>(sc + l.chunks[s]);
+    lp.counts = reinterpret_cast<uint32_t*>(sc + l.counts[s]);
+    lp.prefix = reinterpret_cast<uint64_t*>(sc + l.prefix[s]);
+    lp.status = reinterpret_cast<uint64_t*>(sc + l.status[s]);
+    lp.ctr = &hdr->lv[s];
+    lp.nsegs = reinterpret_cast<SegDesc*>(sc + l.segs[t]);
+    lp.nchunks = reinterpret_cast<ChunkDesc*>(sc + l.chunks[t]);
+    lp.nctr = &hdr->lv[t];
+    lp.max_segs = l.max_segs;
+    lp.max_chunks = l.max_chunks;
+    unsigned char* buf1 = sc + l.pingpong;
+    lp.src = (level & 1u) ? buf1 : buf0;
+    lp.dst = (level & 1u) ? buf0 : buf1;
+    return lp;
+}
+
+static shuf_status check_run_args(shuf_plan_s* p, void* ptr, void* scratch, uint64_t scratch_bytes) {
+    if (!p) return SHUF_ERR_INVALID_ARG;
+    if (p->n > 1 && (!ptr || !scratch)) return SHUF_ERR_INVALID_ARG;
+    if (((uintptr_t)ptr & 15u) || ((uintptr_t)scratch & 15u)) return SHUF_ERR_ALIGNMENT;
+    if (p->n > 1 && scratch_bytes < p->lay.total) return SHUF_ERR_SCRATCH;
+    return SHUF_OK;
+}
+
+// Optional per-launch CUDA-event bracketing (shuf_profile_run only).
+struct Prof {
+    cudaStream_t st;
+    std::vector<int> cls;
+    std::vector<cudaEvent_t> ev;  // 2 per launch
+    cudaError_t mark(int c, bool begin) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r) return r;
+        ev.push_back(e);
+        if (begin) cls.push_back(c);
+        return cudaEventRecord(e, st);
+    }
+    ~Prof() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+#define LAUNCH(cls_, expr)                                  \
+    do {                                                    \
+        if (prof && (e = prof->mark(cls_, true))) return cuda_fail(p, e);  \
+        if ((e = (expr))) return cuda_fail(p, e);           \
+        if (prof && (e = prof->mark(cls_, false))) return cuda_fail(p, e); \
+        ++launches;                                         \
+    } while (0)
+
+// Enqueue the whole shuffle.  segmented: d_offsets != nullptr.
+static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets, uint64_t nsegs, void* scratch,
+                           cudaStream_t st, uint32_t max_levels, int run_leaves, Prof* prof = nullptr) {
+    p->last_launches = 0;
+    cudaError_t e = device_setup(p);
+    if (e) return cuda_fail(p, e);
+    unsigned char* sc = static_cast<unsigned char*>(scratch);
+    unsigned char* buf0 = static_cast<unsigned char*>(ptr);
+    Header* hdr = reinterpret_cast<Header*>(sc + p->lay.header);
+    p->last_hdr = hdr;
+    RunParams rp;
+    rp.buf0 = buf0;
+    rp.buf1 = sc + p->lay.pingpong;
+    rp.hdr = hdr;
+    rp.n = p->n;
+    rp.eb = p->eb;
+    rp.k = p->k;
+    rp.L = p->L;
+    rp.S_fuse = p->S_fuse;
+    rp.chunk = p->chunk;
+    rp.max_levels = max_levels;
+    rp.planned_levels = p->levels;
+    rp.run_leaves = run_leaves;
+    rp.bp = make_bucket_params(p->k);
+    rp.seed = p->seed;
+    uint64_t launches = 0;
+    if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
+    const LevelParams lp0 = level_params(p, sc, buf0, 0);
+    if (d_offsets) {
+        LAUNCH(SHUF_K_INIT, launch_init_segmented(rp, lp0, d_offsets, nsegs, st, p->grid_small));
+        LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, d_offsets, nsegs, st, p->grid_finish));
+    } else {
+        LAUNCH(SHUF_K_INIT, launch_init(rp, lp0, st, p->grid_small));
+        if (p->n <= p->S_fuse) LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
+    }
+    const uint32_t G = p->levels < max_levels ? p->levels : max_levels;
+    for (uint32_t lv = 0; lv < G; ++lv) {
+        const LevelParams lp = level_params(p, sc, buf0, lv);
+        LAUNCH(SHUF_K_HIST, launch_hist(rp, lp, st, p->grid_hist));
+        LAUNCH(SHUF_K_SCAN, launch_scan(rp, lp, st, p->grid_scan));
+        LAUNCH(SHUF_K_PLAN, launch_plan(rp, lp, st, p->grid_small));
+        LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
+        LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
+    }
+    p->last_launches = launches;
+    return SHUF_OK;
+}
+
+extern "C" shuf_status shuf_run(shuf_plan_t p, void* ptr, void* scratch, uint64_t scratch_bytes, void* stream) {
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    if (s) return s;
+    if (p->n <= 1) {
+        p->last_launches = 0;
+        return SHUF_OK;
+    }
+    return enqueue(p, ptr, nullptr, 0, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
+}
+
+extern "C" shuf_status shuf_debug_run_levels(shuf_plan_t p, void* ptr, void* scratch, uint64_t scratch_bytes,
+                                             void* stream, uint32_t max_levels, int run_leaves) {
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    if (s) return s;
+    if (p->n <= 1) return SHUF_OK;
+    return enqueue(p, ptr, nullptr, 0, scratch, static_cast<cudaStream_t>(stream), max_levels, run_leaves ? 1 : 0);
+}
+
+extern "C" shuf_status shuf_segmented(shuf_plan_t p, void* ptr, const uint64_t* d_offsets, uint64_t num_segments,
+                                      void* scratch, uint64_t scratch_bytes, void* stream) {
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    if (s) return s;
+    if (!d_offsets) return SHUF_ERR_INVALID_ARG;
+    if ((uintptr_t)d_offsets & 7u) return SHUF_ERR_ALIGNMENT;
+    if (num_segments == 0 || p->n == 0) {
+        p->last_launches = 0;
+        return SHUF_OK;
+    }
+    return enqueue(p, ptr, d_offsets, num_segments, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
+}
+
+extern "C" shuf_status shuf_profile_run(shuf_plan_t p, void* ptr, const uint64_t* d_offsets, uint64_t num_segments,
+                                        void* scratch, uint64_t scratch_bytes, void* stream, float* ms_by_class,
+                                        uint32_t* launches_by_class) {
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    if (s) return s;
+    if (!ms_by_class || !launches_by_class) return SHUF_ERR_INVALID_ARG;
+    for (int c = 0; c < SHUF_K_CLASSES; ++c) {
+        ms_by_class[c] = 0.f;
+        launches_by_class[c] = 0;
+    }
+    if (p->n <= 1 || (d_offsets && num_segments == 0)) return SHUF_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Prof prof;
+    prof.st = st;
+    s = enqueue(p, ptr, d_offsets, num_segments, scratch, st, 0xFFFFFFFFu, 1, &prof);
+    if (s) return s;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e) return cuda_fail(p, e);
+    for (size_t i = 0; i < prof.cls.size(); ++i) {
+        float ms = 0.f;
+        if ((e = cudaEventElapsedTime(&ms, prof.ev[2 * i], prof.ev[2 * i + 1]))) return cuda_fail(p, e);
+        ms_by_class[prof.cls[i]] += ms;
+        launches_by_class[prof.cls[i]] += 1;
+    }
+    return SHUF_OK;
+}
+
+extern "C" shuf_status shuf_debug_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count, uint32_t k,
+                                               uint32_t* d_out, void* stream) {
+    if (k < 2 || k > 65536 || (!d_out && count)) return SHUF_ERR_INVALID_ARG;
+    if (count == 0) return SHUF_OK;
+    cudaError_t e = launch_debug_bucket_draws(K, level, p0, count, k, d_out, static_cast<cudaStream_t>(stream));
+    return e ? SHUF_ERR_CUDA : SHUF_OK;
+}
+
+extern "C" shuf_status shuf_debug_fy_draws(uint64_t K, const uint64_t* d_P, const uint32_t* d_s, uint64_t count,
+                                           uint32_t* d_out, void* stream) {
+    if (count && (!d_P || !d_s || !d_out)) return SHUF_ERR_INVALID_ARG;
+    if (count == 0) return SHUF_OK;
+    cudaError_t e = launch_debug_fy_draws(K, d_P, d_s, count, d_out, static_cast<cudaStream_t>(stream));
+    return e ? SHUF_ERR_CUDA : SHUF_OK;
+}
+
+extern "C" shuf_status shuf_last_device_error(shuf_plan_t p, void* stream) {
+    if (!p) return SHUF_ERR_INVALID_ARG;
+    if (!p->last_hdr) return SHUF_OK;
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e) return cuda_fail(p, e);
+    uint32_t err = 0;
+    if ((e = cudaMemcpy(&err, &p->last_hdr->error, sizeof err, cudaMemcpyDeviceToHost))) return cuda_fail(p, e);
+    if (err) {
+        uint32_t zero = 0;
+        cudaMemcpy(&p->last_hdr->error, &zero, sizeof zero, cudaMemcpyHostToDevice);
+    }
+    return (shuf_status)err;
+}
+
+extern "C" shuf_status shuf_last_run_stats(shuf_plan_t p, void* stream, uint64_t* out, uint32_t count) {
+    if (!p || !out) return SHUF_ERR_INVALID_ARG;
+    for (uint32_t i = 0; i < count; ++i) out[i] = 0;
+    if (!p->last_hdr) return SHUF_OK;
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e) return cuda_fail(p, e);
+    Header h;
+    if ((e = cudaMemcpy(&h, p->last_hdr, sizeof h, cudaMemcpyDeviceToHost))) return cuda_fail(p, e);
+    // layout: [0] finished, [1] fy_elems, [2 + 2l] hbm(l), [3 + 2l] smem(l)
+    if (count > 0) out[0] = h.finished;
+    if (count > 1) out[1] = h.fy_elems;
+    for (uint32_t l = 0; l < kMaxLevels; ++l) {
+        if (2 + 2 * l < count) out[2 + 2 * l] = h.scattered_hbm[l];
+        if (3 + 2 * l < count) out[3 + 2 * l] = h.scattered_smem[l];
+    }
+    return SHUF_OK;
+}
+
+extern "C" void shuf_destroy(shuf_plan_t p) { delete p; }
+
+extern "C" const char* shuf_status_string(shuf_status s) {
+    switch (s) {
+    case SHUF_OK: return "ok";
+    case SHUF_ERR_INVALID_ARG: return "invalid argument";
+    case SHUF_ERR_UNSUPPORTED: return "unsupported on the device path";
+    case SHUF_ERR_ALIGNMENT: return "pointer not 16-byte aligned";
+    case SHUF_ERR_SCRATCH: return "scratch buffer too small";
+    case SHUF_ERR_DEPTH: return "more scatter levels than planned";
+    case SHUF_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}

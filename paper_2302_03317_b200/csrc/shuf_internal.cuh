@@ -1,0 +1,133 @@
+// Internal descriptors, scratch layout and kernel entry points of libshuf.
+// DESIGN.md section 4 describes the pipeline; section 5 the HBM layout.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "philox.cuh"
+
+namespace shuf {
+
+// ----------------------------------------------------------- constants ----
+constexpr int kWarps = 16;                 // warps per CTA in the ranking kernels
+constexpr int kThreads = kWarps * 32;      // 512
+constexpr uint32_t kTileBytes = 16384;     // one scatter tile (T = kTileBytes / eb elements)
+constexpr uint32_t kMaxK = 1024;           // device bucket-count limit
+constexpr uint32_t kScanTile = 4096;       // entries per decoupled-lookback tile
+constexpr uint32_t kSmemLimit = 227 * 1024;
+constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
+constexpr uint32_t kSegGroup = 8;          // user segments per finish work unit (segmented mode)
+constexpr uint32_t kMaxLevels = 256;
+constexpr uint32_t kFrontierCap = 1024;     // pending in-smem sub-segments per level
+
+// ---------------------------------------------------------- descriptors ---
+// A segment processed by an HBM-resident ("global") scatter level.
+struct SegDesc {
+    uint64_t start;   // first element (absolute index into the buffer)
+    uint64_t len;     // elements
+    uint64_t origin;  // absolute index of the problem's position 0 (D7)
+    uint64_t key;     // K(seed, s)
+    uint64_t cbase;   // first count entry of this segment's (bucket, chunk) block
+    uint32_t nchunks; // chunks of this segment
+    uint32_t pad;
+};
+
+// Chunk j of a level: chunk c of segment seg, positions
+// [start + c*C, min(start + len, start + (c+1)*C)).
+struct ChunkDesc {
+    uint32_t seg;
+    uint32_t c;
+};
+
+// Per-level (two slots, by level parity) device counters.
+struct LevelCounters {
+    uint32_t nseg;
+    uint32_t nchunk;
+    uint32_t scan_ticket;
+    uint32_t pad;
+};
+
+struct Header {
+    LevelCounters lv[2];
+    uint64_t root_off[2];  // {0, n}: the single problem as a one-segment batch
+    uint32_t error;        // latched shuf_status detected on the device
+    uint32_t pad[7];
+    // measurement counters (one atomic per chunk / per shared-memory scatter)
+    uint64_t scattered_hbm[kMaxLevels];   // elements scattered through HBM at level l
+    uint64_t scattered_smem[kMaxLevels];  // elements scattered in shared memory at level l
+    uint64_t finished;                    // elements written by the fused finish
+    uint64_t fy_elems;                    // elements in Fisher-Yates leaves
+};
+
+// Byte offsets of every region inside the caller's scratch buffer.
+struct ScratchLayout {
+    uint64_t pingpong;  // n * eb
+    uint64_t header;
+    uint64_t segs[2];
+    uint64_t chunks[2];
+    uint64_t counts[2];  // u32 per (bucket, chunk)
+    uint64_t prefix[2];  // u64 per (bucket, chunk)
+    uint64_t status[2];  // u64 per scan tile
+    uint64_t total;
+    uint64_t max_segs, max_chunks, max_entries, max_tiles;
+};
+
+// Everything a kernel needs about the run (passed by value).
+struct RunParams {
+    unsigned char* buf0;  // ptr (level-0 input, final output)
+    unsigned char* buf1;  // ping-pong buffer in scratch
+    Header* hdr;
+    uint64_t n;
+    uint32_t eb;
+    uint32_t k;
+    uint32_t L;
+    uint32_t S_fuse;      // max elements of a segment finished in shared memory
+    uint32_t chunk;       // C: elements per chunk (multiple of the tile)
+    uint32_t max_levels;  // debug level limit (0xFFFFFFFF = none)
+    uint32_t planned_levels;
+    int run_leaves;
+    BucketParams bp;
+    uint64_t seed;
+};
+
+struct LevelParams {
+    uint32_t level;     // l
+    int slot;           // l & 1
+    SegDesc* segs;
+    ChunkDesc* chunks;
+    uint32_t* counts;
+    uint64_t* prefix;
+    uint64_t* status;
+    LevelCounters* ctr;
+    // next level (slot ^ 1)
+    SegDesc* nsegs;
+    ChunkDesc* nchunks;
+    LevelCounters* nctr;
+    uint64_t max_segs, max_chunks;
+    unsigned char* src;  // level input buffer
+    unsigned char* dst;  // level output buffer
+};
+
+// ------------------------------------------------------ host launchers ---
+cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid);
+cudaError_t launch_init_segmented(const RunParams& rp, const LevelParams& lp0, const uint64_t* d_offsets,
+                                  uint64_t num_segments, cudaStream_t s, int grid);
+cudaError_t launch_hist(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_scan(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_plan(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_finish_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
+                                   cudaStream_t s, int grid);
+uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k);
+uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);
+cudaError_t configure_scatter(uint32_t smem);
+cudaError_t configure_finish(uint32_t smem);
+cudaError_t occupancy_level(uint32_t eb, uint32_t k, int* hist, int* scan, int* scatter);
+cudaError_t occupancy_finish(uint32_t eb, uint32_t smem, int* blocks);
+cudaError_t launch_debug_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count, uint32_t k,
+                                      uint32_t* d_out, cudaStream_t s);
+cudaError_t launch_debug_fy_draws(uint64_t K, const uint64_t* d_P, const uint32_t* d_s, uint64_t count,
+                                  uint32_t* d_out, cudaStream_t s);
+
+}  // namespace shuf

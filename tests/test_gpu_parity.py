@@ -1,0 +1,115 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, bit-exact (integer work: DESIGN.md section 6)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2302_03317_b200 as shuf  # noqa: E402
+from tests.gpu_util import gpu_segmented, gpu_shuffle, to_dev, to_host  # noqa: E402
+
+
+# ------------------------------------------------------------ raw draws --
+@pytest.mark.parametrize("k", [2, 3, 7, 64, 256, 1000, 1024, 40000, 65536])
+@pytest.mark.parametrize("level,p0", [(0, 0), (1, 12345), (2, 2**33 + 5), (255, 2**40 - 3)])
+def test_raw_bucket_draws(k, level, p0):
+    K = oracle.problem_key(9, 4)
+    count = 5000
+    out = torch.empty(count, dtype=torch.int32, device="cuda")
+    shuf.shuf_debug_bucket_draws(K, level, p0, count, k, out)
+    got = out.cpu().numpy().view(np.uint32)
+    exp = oracle.bucket_draws(K, level, p0, count, k)
+    assert (got == exp).all()
+
+
+def test_raw_fy_draws_including_forced_retries():
+    K = oracle.problem_key(11, 2)
+    rng = np.random.default_rng(5)
+    P = np.concatenate([np.arange(3000), rng.integers(0, 2**50, size=3000)]).astype(np.uint64)
+    s = np.concatenate([np.arange(2, 3002), rng.integers(2, 2**32, size=2000), np.full(1000, 2**31 + 1)])
+    s = s.astype(np.uint32)
+    out = torch.empty(P.shape[0], dtype=torch.int32, device="cuda")
+    shuf.shuf_debug_fy_draws(K, to_dev(P), to_dev(s), out)
+    got = out.cpu().numpy().view(np.uint32)
+    exp = oracle.fy_draws(K, P, s)
+    assert (got == exp).all()
+    # the s = 2^31+1 block rejects about half of its primary words
+    assert sum(oracle.fy_draw(K, int(p), 2**31 + 1)[1] > 0 for p in P[-1000:]) > 300
+
+
+# ------------------------------------------------------- end to end ------
+CASES = [
+    # n, k, L, seed, eb -- several tiles, ragged tails, every path
+    (2, 2, 1, 1, 4), (3, 4, 2, 2, 4), (1000, 256, 4096, 3, 4),          # root leaf (FY only)
+    (5000, 16, 100, 4, 4),                                              # root fused in smem
+    (100_003, 256, 4096, 5, 4),                                         # 1 global level + fused
+    (1 << 20, 256, 4096, 1, 4),                                         # config 1
+    (777_777, 7, 300, 6, 4),                                            # non-power-of-two k
+    (300_001, 1000, 50, 7, 4),                                          # k with rejections
+    (200_000, 2, 1, 8, 4),                                              # deepest recursion
+    (123_457, 64, 2048, 9, 8), (99_991, 1024, 2048, 10, 16),            # element sizes
+    (3_000_000, 256, 4096, 11, 4),                                      # 2 global levels
+]
+
+
+def make(n, eb, seed=0):
+    if eb == 4:
+        return np.arange(n, dtype=np.uint32)
+    if eb == 8:
+        return synth.splitmix64_stream_np(3 + seed, 0, n)
+    return synth.make_input_np(synth.WORKLOADS["c4"], n=n)
+
+
+@pytest.mark.parametrize("n,k,L,seed,eb", CASES)
+def test_shuffle_bit_exact(n, k, L, seed, eb):
+    a = make(n, eb)
+    got = gpu_shuffle(a, k, L, seed)
+    exp = oracle.shuffle(a, k, L, seed)
+    assert (got == exp).all()
+
+
+@pytest.mark.parametrize("n,k,L,seed", [(100_003, 256, 300, 5), (2_000_000, 64, 40, 3), (50_000, 2, 5, 2)])
+@pytest.mark.parametrize("max_levels", [0, 1, 2, 3])
+@pytest.mark.parametrize("run_leaves", [False, True])
+def test_level_limited_state_matches(n, k, L, seed, max_levels, run_leaves):
+    """Kernel-level parity: stop after levels l < max_levels (in HBM or in
+    shared memory alike) and compare the intermediate state."""
+    a = np.arange(n, dtype=np.uint32)
+    got = gpu_shuffle(a, k, L, seed, max_levels=max_levels, run_leaves=run_leaves)
+    exp = oracle.shuffle(a, k, L, seed, max_levels=max_levels, run_leaves=run_leaves)
+    assert (got == exp).all()
+
+
+def test_segmented_bit_exact_with_edge_segments():
+    lens = np.array([0, 1, 2, 5, 4095, 4096, 4097, 30_000, 0, 70_000, 3, 250_000, 1, 0])
+    off = synth.segment_offsets(lens)
+    a = synth.make_input_np(synth.WORKLOADS["c5"], offsets=off)
+    got = gpu_segmented(a, off, 64, 4096, 5)
+    exp = oracle.segmented(a, off, 64, 4096, 5)
+    assert (got == exp).all()
+
+
+def test_segmented_c5_shape_sample():
+    lens = synth.c5_lengths(4096)
+    off = synth.segment_offsets(lens)
+    a = synth.make_input_np(synth.WORKLOADS["c5"], offsets=off)
+    got = gpu_segmented(a, off, 64, 4096, 5)
+    exp = oracle.segmented(a, off, 64, 4096, 5)
+    assert (got == exp).all()
+
+
+def test_repeat_runs_identical_and_stream_independent():
+    a = np.arange(1_500_000, dtype=np.uint32)
+    r1 = gpu_shuffle(a, 256, 4096, 42)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        r2 = gpu_shuffle(a, 256, 4096, 42)
+    assert (r1 == r2).all()
+    assert (np.sort(r1) == a).all()
