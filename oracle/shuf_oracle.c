@@ -14,7 +14,9 @@
  *                              north star; the paper's own RNG is Pcg64Mcg)
  *   D4 bucket draw .......... Lemire bounded integer, "sampling an
  *                              integer from [0,s) with s=2^k ... shifting and
- *                              masking"; rejection for general s (Lemire 2019)
+ *                              masking"; rejection for general s (Lemire 2019);
+ *                              8-bit lanes (16 draws per Philox call) for
+ *                              power-of-two k <= 256, 16-bit lanes otherwise
  *   D5 Fisher-Yates draw .... Fig. 1: gen_index(rng, i+1),
  *                              "partner from [0..i]"
  *   D6 recursion ............ ScatterShuffle, IpSc "groups X by A
@@ -101,14 +103,44 @@ int oracle_lemire32_accept(uint32_t w, uint32_t s, uint32_t *out)
 
 /* ---------------------------------------------------------------- D4 ---- */
 #define TAG_SC 1u
-#define TAG_FY 2u
+#define TAG_FY16 2u
 #define TAG_SC_RETRY 3u
-#define TAG_FY_RETRY 4u
+#define TAG_FY16_RETRY 4u
+#define TAG_FY32 5u
+#define TAG_FY32_RETRY 6u
 
+/* log2(k) if k is a power of two <= 256 (8-bit lanes), else -1 (16-bit lanes) */
+static int narrow_shift(uint32_t k)
+{
+    if (k > 256u || (k & (k - 1u)) != 0)
+        return -1;
+    int b = 0;
+    while ((1u << b) < k)
+        b++;
+    return b;
+}
+
+/* D4: bucket of problem-relative position p at level `level`.
+ * Power-of-two k <= 256: 16 draws per Philox call, 8-bit lane p&15 of
+ *   Philox(K, (p>>4, level, SC)), bucket = lane >> (8 - log2 k) (shift only).
+ * Otherwise: 8 draws per call, 16-bit lane p&7 of Philox(K, (p>>3, level, SC)),
+ *   Lemire with rejection; retries from Philox(K, (p, level|a<<8, SC_RETRY)). */
 uint32_t oracle_bucket_draw(uint64_t K, uint32_t level, uint64_t p, uint32_t k, uint64_t *rejections)
 {
     uint32_t key[2], ctr[4], w[4], out;
     key_words(K, key);
+    int b = narrow_shift(k);
+    if (b >= 0) {
+        uint64_t g = p >> 4;
+        ctr[0] = (uint32_t)g;
+        ctr[1] = (uint32_t)(g >> 32);
+        ctr[2] = level;
+        ctr[3] = TAG_SC;
+        oracle_philox4x32_10(ctr, key, w);
+        uint32_t j = (uint32_t)(p & 15u);
+        uint32_t v = (w[j >> 2] >> (8u * (j & 3u))) & 0xFFu;
+        return v >> (8 - b);
+    }
     uint64_t g = p >> 3;
     ctr[0] = (uint32_t)g;
     ctr[1] = (uint32_t)(g >> 32);
@@ -134,15 +166,44 @@ uint32_t oracle_bucket_draw(uint64_t K, uint32_t level, uint64_t p, uint32_t k, 
 }
 
 /* ---------------------------------------------------------------- D5 ---- */
+/* D5: Fisher-Yates partner for the step at problem-relative position P with
+ * bound s = i+1 (Fig. 1: gen_index(rng, i+1), "partner from [0..i]").
+ * s <= 2^16: 16-bit lane P&7 of Philox(K, (P>>3, 0, FY16)), Lemire16, retries
+ *   from Philox(K, (P, a, FY16_RETRY)).w0 & 0xFFFF.
+ * s >  2^16: 32-bit word P&3 of Philox(K, (P>>2, 0, FY32)), Lemire32, retries
+ *   from Philox(K, (P, a, FY32_RETRY)).w0. */
 uint32_t oracle_fy_draw(uint64_t K, uint64_t P, uint32_t s, uint64_t *rejections)
 {
     uint32_t key[2], ctr[4], w[4], out;
     key_words(K, key);
+    if (s <= 65536u) {
+        uint64_t g = P >> 3;
+        ctr[0] = (uint32_t)g;
+        ctr[1] = (uint32_t)(g >> 32);
+        ctr[2] = 0;
+        ctr[3] = TAG_FY16;
+        oracle_philox4x32_10(ctr, key, w);
+        uint32_t j = (uint32_t)(P & 7u);
+        uint32_t v = (w[j >> 1] >> (16u * (j & 1u))) & 0xFFFFu;
+        if (oracle_lemire16_accept(v, s, &out))
+            return out;
+        for (uint32_t a = 1;; a++) {
+            if (rejections)
+                (*rejections)++;
+            ctr[0] = (uint32_t)P;
+            ctr[1] = (uint32_t)(P >> 32);
+            ctr[2] = a;
+            ctr[3] = TAG_FY16_RETRY;
+            oracle_philox4x32_10(ctr, key, w);
+            if (oracle_lemire16_accept(w[0] & 0xFFFFu, s, &out))
+                return out;
+        }
+    }
     uint64_t g = P >> 2;
     ctr[0] = (uint32_t)g;
     ctr[1] = (uint32_t)(g >> 32);
     ctr[2] = 0;
-    ctr[3] = TAG_FY;
+    ctr[3] = TAG_FY32;
     oracle_philox4x32_10(ctr, key, w);
     if (oracle_lemire32_accept(w[P & 3u], s, &out))
         return out;
@@ -152,7 +213,7 @@ uint32_t oracle_fy_draw(uint64_t K, uint64_t P, uint32_t s, uint64_t *rejections
         ctr[0] = (uint32_t)P;
         ctr[1] = (uint32_t)(P >> 32);
         ctr[2] = a;
-        ctr[3] = TAG_FY_RETRY;
+        ctr[3] = TAG_FY32_RETRY;
         oracle_philox4x32_10(ctr, key, w);
         if (oracle_lemire32_accept(w[0], s, &out))
             return out;

@@ -26,11 +26,23 @@ def philox_np(c0, c1, c2, c3, k0: int, k1: int):
     return x0, x1, x2, x3
 
 
+def _narrow_shift(k: int):
+    return (k.bit_length() - 1) if (k <= 256 and k & (k - 1) == 0) else -1
+
+
 def bucket_np(K: int, level: int, p: np.ndarray, k: int) -> np.ndarray:
     p = np.asarray(p, dtype=np.uint64)
+    kw = (K & 0xFFFFFFFF, K >> 32)
+    b = _narrow_shift(k)
+    if b >= 0:
+        g = p >> np.uint64(4)
+        W = np.stack(philox_np(g & M32, g >> np.uint64(32), np.uint64(level), np.uint64(1), *kw))
+        j = (p & np.uint64(15)).astype(np.int64)
+        word = W[j >> 2, np.arange(p.shape[0])]
+        v = (word >> (np.uint64(8) * (j & 3).astype(np.uint64))) & np.uint64(0xFF)
+        return (v >> np.uint64(8 - b)).astype(np.int64)
     g = p >> np.uint64(3)
-    w = philox_np(g & M32, g >> np.uint64(32), np.uint64(level), np.uint64(1), K & 0xFFFFFFFF, K >> 32)
-    W = np.stack(w)  # 4 x n
+    W = np.stack(philox_np(g & M32, g >> np.uint64(32), np.uint64(level), np.uint64(1), *kw))
     j = (p & np.uint64(7)).astype(np.int64)
     word = W[j >> 1, np.arange(p.shape[0])]
     v = (word >> (np.uint64(16) * (j & 1).astype(np.uint64))) & np.uint64(0xFFFF)
@@ -42,10 +54,8 @@ def bucket_np(K: int, level: int, p: np.ndarray, k: int) -> np.ndarray:
     while bad.any():
         a += 1
         pb = p[bad]
-        w0 = philox_np(pb & M32, pb >> np.uint64(32), np.uint64(level | (a << 8)), np.uint64(3),
-                       K & 0xFFFFFFFF, K >> 32)[0]
-        vb = w0 & np.uint64(0xFFFF)
-        mb = vb * np.uint64(k)
+        w0 = philox_np(pb & M32, pb >> np.uint64(32), np.uint64(level | (a << 8)), np.uint64(3), *kw)[0]
+        mb = (w0 & np.uint64(0xFFFF)) * np.uint64(k)
         idx = np.nonzero(bad)[0]
         ok = (mb & np.uint64(0xFFFF)) >= t
         out[idx[ok]] = (mb[ok] >> np.uint64(16)).astype(np.int64)
@@ -54,12 +64,16 @@ def bucket_np(K: int, level: int, p: np.ndarray, k: int) -> np.ndarray:
 
 
 def fy_np(K: int, P: np.ndarray, s: np.ndarray) -> np.ndarray:
+    """D5 for bounds s <= 2^16 (16-bit lanes; the only case leaves <= 65536 need)."""
     P = np.asarray(P, dtype=np.uint64)
     s = np.asarray(s, dtype=np.uint64)
-    g = P >> np.uint64(2)
-    W = np.stack(philox_np(g & M32, g >> np.uint64(32), np.uint64(0), np.uint64(2), K & 0xFFFFFFFF, K >> 32))
-    w = W[(P & np.uint64(3)).astype(np.int64), np.arange(P.shape[0])]
-    t = (np.uint64(2**32) % s) if s.size else s
+    assert (s <= 65536).all()
+    kw = (K & 0xFFFFFFFF, K >> 32)
+    g = P >> np.uint64(3)
+    W = np.stack(philox_np(g & M32, g >> np.uint64(32), np.uint64(0), np.uint64(2), *kw))
+    j = (P & np.uint64(7)).astype(np.int64)
+    v = (W[j >> 1, np.arange(P.shape[0])] >> (np.uint64(16) * (j & 1).astype(np.uint64))) & np.uint64(0xFFFF)
+    t = np.uint64(65536) % np.maximum(s, np.uint64(1))
     out = np.zeros(P.shape[0], dtype=np.int64)
     todo = np.ones(P.shape[0], dtype=bool)
     a = 0
@@ -67,15 +81,12 @@ def fy_np(K: int, P: np.ndarray, s: np.ndarray) -> np.ndarray:
         idx = np.nonzero(todo)[0]
         if a:
             Pb = P[idx]
-            w_i = philox_np(Pb & M32, Pb >> np.uint64(32), np.uint64(a), np.uint64(4), K & 0xFFFFFFFF, K >> 32)[0]
+            v_i = philox_np(Pb & M32, Pb >> np.uint64(32), np.uint64(a), np.uint64(4), *kw)[0] & np.uint64(0xFFFF)
         else:
-            w_i = w[idx]
-        # 64-bit product of two < 2^32 values; python ints avoid overflow
-        M = np.array([int(x) * int(y) for x, y in zip(w_i, s[idx])], dtype=object)
-        lo = np.array([int(m) & 0xFFFFFFFF for m in M], dtype=np.uint64)
-        hi = np.array([int(m) >> 32 for m in M], dtype=np.int64)
-        ok = lo >= t[idx]
-        out[idx[ok]] = hi[ok]
+            v_i = v[idx]
+        m = v_i * s[idx]
+        ok = (m & np.uint64(0xFFFF)) >= t[idx]
+        out[idx[ok]] = (m[ok] >> np.uint64(16)).astype(np.int64)
         todo[idx[ok]] = False
         a += 1
     return out

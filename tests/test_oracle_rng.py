@@ -104,17 +104,22 @@ def test_lemire32_power_of_two_never_rejects():
 
 
 def test_bucket_draw_layout_first_principles():
-    """D4 lanes: the 8 draws of a group g are the 16-bit halves of Philox(K,
-    (g, level, SC=1)) little-endian, mapped through Lemire (power-of-two k:
-    top log2(k) bits)."""
+    """D4 lanes for power-of-two k <= 256: the 16 draws of group g are the
+    8-bit lanes of Philox(K, (g, level, SC=1)) little-endian, top log2(k)
+    bits (shift only); for k > 256 the 8 draws of group g are the
+    16-bit lanes of the same counter (level, SC)."""
     K = oracle.problem_key(9, 0)
     key = [K & 0xFFFFFFFF, K >> 32]
     for level in (0, 3):
         for g in (0, 1, 12345, 2**33 + 7):
             w = oracle.philox([g & 0xFFFFFFFF, g >> 32, level, 1], key)
-            lanes = [(int(w[j >> 1]) >> (16 * (j & 1))) & 0xFFFF for j in range(8)]
-            draws = oracle.bucket_draws(K, level, 8 * g, 8, 256)
-            assert list(draws) == [v >> 8 for v in lanes]
+            b8 = [(int(w[j >> 2]) >> (8 * (j & 3))) & 0xFF for j in range(16)]
+            assert list(oracle.bucket_draws(K, level, 16 * g, 16, 256)) == b8
+            assert list(oracle.bucket_draws(K, level, 16 * g, 16, 64)) == [v >> 2 for v in b8]
+            assert list(oracle.bucket_draws(K, level, 16 * g, 16, 2)) == [v >> 7 for v in b8]
+            l16 = [(int(w[j >> 1]) >> (16 * (j & 1))) & 0xFFFF for j in range(8)]
+            assert list(oracle.bucket_draws(K, level, 8 * g, 8, 1024)) == [v >> 6 for v in l16]
+            assert list(oracle.bucket_draws(K, level, 8 * g, 8, 65536)) == l16
 
 
 def test_bucket_draw_retry_stream():
@@ -139,23 +144,54 @@ def test_bucket_draw_retry_stream():
     assert found > 500
 
 
-def test_fy_draw_layout_and_retry():
-    """D5: primary word = Philox(K, (P>>2, 0, FY=2))[P&3]; retries from
-    Philox(K, (P, a, FY_RETRY=4)).w0; bound s=2^31+1 rejects ~half the words."""
+def test_fy_draw_layout_and_retry_16bit():
+    """D5, s <= 2^16: 16-bit lane P&7 of Philox(K, (P>>3, 0, FY16=2));
+    retries from Philox(K, (P, a, FY16_RETRY=4)).w0 & 0xFFFF; s=40000
+    rejects ~39% of the lanes."""
+    K = oracle.problem_key(11, 2)
+    key = [K & 0xFFFFFFFF, K >> 32]
+    s = 40000
+    t = 65536 % s
+    seen = 0
+    for P in list(range(400)) + [2**40 + 3]:
+        j, rej = oracle.fy_draw(K, P, s)
+        g = P >> 3
+        w = oracle.philox([g & 0xFFFFFFFF, g >> 32, 0, 2], key)
+        v = (int(w[(P & 7) >> 1]) >> (16 * (P & 1))) & 0xFFFF
+        a = 0
+        while (v * s) & 0xFFFF < t:
+            a += 1
+            v = int(oracle.philox([P & 0xFFFFFFFF, P >> 32, a, 4], key)[0]) & 0xFFFF
+        assert rej == a and j == (v * s) >> 16 and 0 <= j < s
+        seen += rej > 0
+    assert seen > 80
+
+
+def test_fy_draw_layout_and_retry_32bit():
+    """D5, s > 2^16: 32-bit word P&3 of Philox(K, (P>>2, 0, FY32=5)); retries
+    from Philox(K, (P, a, FY32_RETRY=6)).w0; s=2^31+1 rejects ~half."""
     K = oracle.problem_key(11, 2)
     key = [K & 0xFFFFFFFF, K >> 32]
     s = 2**31 + 1
     t = 2**32 % s
-    seen_retry = 0
+    seen = 0
     for P in list(range(300)) + [2**40 + 3]:
         j, rej = oracle.fy_draw(K, P, s)
         g = P >> 2
-        w = int(oracle.philox([g & 0xFFFFFFFF, g >> 32, 0, 2], key)[P & 3])
+        w = int(oracle.philox([g & 0xFFFFFFFF, g >> 32, 0, 5], key)[P & 3])
         a = 0
         while (w * s) % 2**32 < t:
             a += 1
-            w = int(oracle.philox([P & 0xFFFFFFFF, P >> 32, a, 4], key)[0])
-        assert rej == a and j == (w * s) >> 32
-        assert 0 <= j < s
-        seen_retry += rej > 0
-    assert seen_retry > 50
+            w = int(oracle.philox([P & 0xFFFFFFFF, P >> 32, a, 6], key)[0])
+        assert rej == a and j == (w * s) >> 32 and 0 <= j < s
+        seen += rej > 0
+    assert seen > 50
+
+
+def test_fy_draw_boundary_65536_uses_16bit_lanes():
+    K = oracle.problem_key(1, 0)
+    key = [K & 0xFFFFFFFF, K >> 32]
+    for P in range(64):
+        w = oracle.philox([(P >> 3), 0, 0, 2], key)
+        v = (int(w[(P & 7) >> 1]) >> (16 * (P & 1))) & 0xFFFF
+        assert oracle.fy_draw(K, P, 65536) == (v, 0)  # s = 2^16: pure shift, no rejection
