@@ -135,6 +135,14 @@ int shuf_last_cuda_error(shuf_plan_t p);
 /* Number of kernel launches the last shuf_run/shuf_segmented enqueued. */
 uint64_t shuf_last_launch_count(shuf_plan_t p);
 
+/* Which in-warp ranking the device path uses (block_ops.cuh): 1 = one
+ * shared-memory atomicAdd per element (same-address atomics of a warp
+ * instruction return in lane order -- verified by a probe kernel at the
+ * first run, since the PTX ISA leaves that order unspecified), 0 = the
+ * documented __match_any_sync path, -1 = not probed yet.  The environment
+ * variable SHUF_RANK_MODE=atomic|match forces one of them. */
+int shuf_rank_mode(void);
+
 /* Planned number of HBM (global) scatter levels for this plan. */
 uint32_t shuf_planned_levels(shuf_plan_t p);
 

@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "shuf_plan", "shuf_last_status", "shuf_scratch_bytes", "shuf_run", "shuf_segmented", "shuf_debug_run_levels",
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
-    "shuf_last_run_stats",
+    "shuf_last_run_stats", "shuf_rank_mode",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish"]
 
@@ -86,6 +86,7 @@ def lib():
         L.shuf_profile_run.restype = i32
         L.shuf_last_run_stats.argtypes = [vp, vp, vp, u32]
         L.shuf_last_run_stats.restype = i32
+        L.shuf_rank_mode.restype = i32
         L.shuf_status_string.argtypes = [i32]
         L.shuf_status_string.restype = ctypes.c_char_p
         _lib = L

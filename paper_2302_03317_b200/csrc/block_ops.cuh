@@ -1,6 +1,17 @@
 // CTA-wide building blocks shared by the scatter and finish kernels:
-// draw generation into shared memory, warp match/ballot stable ranking,
-// block exclusive scan.  (CUDA path only; the oracle never includes this.)
+// draw generation into shared memory, stable in-warp ranking, the
+// bucket-major scan of per-warp counters.  (CUDA path only.)
+//
+// Stable ranking.  A warp walks its sub-tile in rounds of
+// 32 consecutive elements, lane order = position order.  Each lane adds 1 to
+// its bucket's counter in the warp's own counter table with ONE shared-memory
+// atomicAdd; the value returned is the element's rank among the warp's
+// elements of that bucket so far.  This is stable because same-address
+// atomics of one warp instruction return in ascending lane order on this GPU:
+// the PTX ISA leaves that order unspecified, so the library checks it at
+// setup with a probe kernel (k_rank_order_probe) and otherwise uses the
+// documented __match_any_sync path (rank = count + popc(peers & lanemask_lt)).
+// Counters are u16 halves of u32 words (bucket b -> word b>>1, half b&1).
 #pragma once
 #include <cstdint>
 
@@ -10,7 +21,6 @@
 
 namespace shuf {
 
-// Element vector types by element size.
 template <int EB> struct ElemT;
 template <> struct ElemT<4> { using type = uint32_t; };
 template <> struct ElemT<8> { using type = uint2; };
@@ -26,62 +36,129 @@ __device__ __forceinline__ uint32_t warp_inclusive_sum(uint32_t v) {
     return v;
 }
 
-// Exclusive scan of a[0..N) (in shared memory) in place; returns the total.
-// `wsum` is shared scratch of at least kWarps+1 words.  All threads call it.
-template <typename T>
-__device__ uint32_t block_exclusive_scan(T* a, uint32_t N, uint32_t* wsum) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t per = (N + kThreads - 1) / kThreads;
-    const uint32_t beg = min(N, tid * per), end = min(N, beg + per);
-    uint32_t s = 0;
-    for (uint32_t i = beg; i < end; ++i) s += a[i];
-    uint32_t incl = warp_inclusive_sum(s);
+// Exclusive scan over one value per thread; returns the thread's exclusive
+// prefix, *total gets the block total.  wsum: shared scratch of NT/32+1 words.
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t v, uint32_t* wsum, uint32_t* total) {
+    constexpr int NW = NT / 32;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t incl = warp_inclusive_sum(v);
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t v = lane < (uint32_t)kWarps ? wsum[lane] : 0u;
-        uint32_t vi = warp_inclusive_sum(v);
-        if (lane < (uint32_t)kWarps) wsum[lane] = vi - v;
-        if (lane == kWarps - 1) wsum[kWarps] = vi;
+        const uint32_t x = lane < (uint32_t)NW ? wsum[lane] : 0u;
+        const uint32_t xi = warp_inclusive_sum(x);
+        if (lane < (uint32_t)NW) wsum[lane] = xi - x;
+        if (lane == NW - 1) wsum[NW] = xi;
     }
     __syncthreads();
-    uint32_t run = wsum[warp] + incl - s;
-    for (uint32_t i = beg; i < end; ++i) {
-        T t = a[i];
-        a[i] = (T)run;
-        run += t;
-    }
-    const uint32_t total = wsum[kWarps];
+    const uint32_t r = wsum[warp] + incl - v;
+    *total = wsum[NW];
     __syncthreads();
-    return total;
+    return r;
 }
 
-// D4 draws of the problem-relative positions [P0, P0 + m) into d[0..m)
-// (one Philox call per 8 consecutive positions, blocked by thread).
-__device__ __forceinline__ void draws_to_smem(uint16_t* d, uint64_t P0, uint32_t m, PhiloxKey key, uint32_t level,
-                                              BucketParams bp) {
-    if (m == 0) return;
-    const uint64_t g0 = P0 >> 3, g1 = (P0 + m - 1) >> 3;
-    const uint32_t ng = (uint32_t)(g1 - g0 + 1);
-    for (uint32_t t = threadIdx.x; t < ng; t += kThreads) {
+// Draw array in shared memory for positions [P0, P0+m): index of position p
+// is p - base with base = P0 rounded down to a Philox group; narrow draws
+// are u8, wide draws u16.  One Philox call per group, stored with one
+// 16-byte store when the group lies inside the range.
+struct DrawView {
+    unsigned char* d;
+    uint32_t off;     // P0 - base
+    uint32_t narrow;
+    __device__ __forceinline__ uint32_t at(uint32_t e) const {
+        return narrow ? (uint32_t)d[e + off] : (uint32_t)reinterpret_cast<const uint16_t*>(d)[e + off];
+    }
+};
+
+template <int NT>
+__device__ __forceinline__ DrawView draws_to_smem(unsigned char* d, uint64_t P0, uint32_t m, PhiloxKey key,
+                                                  uint32_t level, const BucketParams& bp) {
+    const uint32_t sh = bp.narrow ? 4u : 3u, dpg = 1u << sh;
+    const uint64_t g0 = P0 >> sh;
+    DrawView v{d, (uint32_t)(P0 - (g0 << sh)), bp.narrow};
+    if (m == 0) return v;
+    const uint32_t ng = (uint32_t)(((P0 + m - 1) >> sh) - g0 + 1);
+    for (uint32_t t = threadIdx.x; t < ng; t += NT) {
         const uint64_t g = g0 + t;
         const uint4 w = bucket_group_words(key, level, g);
-        const uint64_t pbase = g << 3;
-        if (pbase >= P0 && pbase + 8 <= P0 + m) {
-            // full group: 8 draws
-            uint32_t b[8];
-#pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) b[j] = bucket_from_lane(lane16(w, j), key, level, pbase + j, bp);
-            uint16_t* out = d + (pbase - P0);
-#pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) out[j] = (uint16_t)b[j];
+        const uint64_t pb = g << sh;
+        if (bp.narrow && bp.shift == 0) {  // k = 256: the lanes are the buckets
+            *reinterpret_cast<uint4*>(d + (size_t)t * 16) = w;
+        } else if (bp.narrow) {
+            const uint32_t s = bp.shift, msk = (0xFFu >> s) * 0x01010101u;
+            *reinterpret_cast<uint4*>(d + (size_t)t * 16) =
+                make_uint4((w.x >> s) & msk, (w.y >> s) & msk, (w.z >> s) & msk, (w.w >> s) & msk);
         } else {
-            for (uint32_t j = 0; j < 8; ++j) {
-                const uint64_t p = pbase + j;
-                if (p >= P0 && p < P0 + m) d[p - P0] = (uint16_t)bucket_from_lane(lane16(w, j), key, level, p, bp);
+            uint32_t b[8];
+            if (pb >= P0 && pb + dpg <= P0 + m) {
+#pragma unroll
+                for (uint32_t j = 0; j < 8; ++j) b[j] = bucket_from_group(w, j, key, level, pb + j, bp);
+            } else {
+#pragma unroll
+                for (uint32_t j = 0; j < 8; ++j)
+                    b[j] = (pb + j >= P0 && pb + j < P0 + m) ? bucket_from_group(w, j, key, level, pb + j, bp) : 0u;
             }
+            *reinterpret_cast<uint4*>(d + (size_t)t * 16) =
+                make_uint4(b[0] | (b[1] << 16), b[2] | (b[3] << 16), b[4] | (b[5] << 16), b[6] | (b[7] << 16));
         }
     }
+    return v;
+}
+
+// Bytes of draw storage for m positions (plus one group of slack on each side).
+__host__ __device__ inline uint32_t draw_bytes(uint32_t m) { return 2u * (m + 32u); }
+
+// Stable rank of this lane's element among the warp's elements of bucket b
+// processed so far; Cw = the warp's packed u16 counters.  All 32 lanes call.
+__device__ __forceinline__ uint32_t warp_rank(uint32_t* Cw, uint32_t b, bool valid, bool ordered) {
+    if (ordered) {
+        if (!valid) return 0u;
+        const uint32_t sh = (b & 1u) << 4;
+        const uint32_t old = atomicAdd(&Cw[b >> 1], 1u << sh);
+        return (old >> sh) & 0xFFFFu;
+    }
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu);
+    uint32_t old = 0;
+    if (valid) old = (Cw[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu;
+    __syncwarp();
+    if (valid && (peers & lanemask_lt()) == 0)
+        atomicAdd(&Cw[b >> 1], (uint32_t)__popc(peers) << ((b & 1u) << 4));
+    __syncwarp();
+    return old + __popc(peers & lanemask_lt());
+}
+
+// C holds nw packed-u16 counter tables of k entries (table w at C + w*kw,
+// kw = ceil(k/2) words).  Replace every count by its exclusive prefix in
+// (bucket, warp) order and write bucket starts to bst[0..k] (bst[k] = total).
+// Requires kw <= NT.  All NT threads call.
+template <int NT>
+__device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum) {
+    const uint32_t x = threadIdx.x;  // word = buckets 2x, 2x+1
+    const uint32_t kw = (k + 1) >> 1;
+    uint32_t t0 = 0, t1 = 0;
+    if (x < kw) {
+        for (uint32_t w = 0; w < nw; ++w) {
+            const uint32_t c = C[w * kw + x];
+            t0 += c & 0xFFFFu;
+            t1 += c >> 16;
+        }
+    }
+    uint32_t total;
+    const uint32_t run = block_exclusive_sum<NT>(t0 + t1, wsum, &total);
+    if (x < kw) {
+        bst[2 * x] = run;
+        if (2 * x + 1 < k) bst[2 * x + 1] = run + t0;
+        uint32_t r0 = run, r1 = run + t0;
+        for (uint32_t w = 0; w < nw; ++w) {
+            const uint32_t c = C[w * kw + x];
+            C[w * kw + x] = (r0 & 0xFFFFu) | (r1 << 16);
+            r0 += c & 0xFFFFu;
+            r1 += c >> 16;
+        }
+    }
+    if (x == 0) bst[k] = total;
+    __syncthreads();
 }
 
 }  // namespace shuf

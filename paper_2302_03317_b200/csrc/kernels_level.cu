@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
         lp.nctr->nchunk = 0;
     }
     const uint32_t k = rp.k;
+    const BucketParams bp = rp.bp;
+    const uint32_t sh = bp.narrow ? 4u : 3u, dpg = 1u << sh;
     for (uint32_t j = blockIdx.x; j < nchunk; j += gridDim.x) {
         for (uint32_t b = threadIdx.x; b < k; b += kThreads) hist[b] = 0;
         __syncthreads();
@@ -99,19 +101,26 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
         const SegDesc sg = lp.segs[ch.seg];
         const uint64_t q0 = sg.start + (uint64_t)ch.c * rp.chunk;
         const uint64_t q1 = min(sg.start + sg.len, q0 + rp.chunk);
-        const uint64_t P0 = q0 - sg.origin, m = q1 - q0;
+        const uint64_t P0 = q0 - sg.origin, P1 = q1 - sg.origin;
         const PhiloxKey key = make_key(sg.key);
-        const uint64_t g0 = P0 >> 3, ng = ((P0 + m - 1) >> 3) - g0 + 1;
+        const uint64_t g0 = P0 >> sh, ng = ((P1 - 1) >> sh) - g0 + 1;
         for (uint64_t t = threadIdx.x; t < ng; t += kThreads) {
             const uint64_t g = g0 + t;
             const uint4 w = bucket_group_words(key, lp.level, g);
-            const uint64_t pb = g << 3;
+            const uint64_t pb = g << sh;
+            if (pb >= P0 && pb + dpg <= P1) {
+                if (bp.narrow) {
 #pragma unroll
-            for (uint32_t jj = 0; jj < 8; ++jj) {
-                const uint64_t p = pb + jj;
-                if (p >= P0 && p < P0 + m) {
-                    const uint32_t b = bucket_from_lane(lane16(w, jj), key, lp.level, p, rp.bp);
-                    atomicAdd(&hist[b], 1u);
+                    for (uint32_t jj = 0; jj < 16; ++jj) atomicAdd(&hist[lane8(w, jj) >> bp.shift], 1u);
+                } else {
+#pragma unroll
+                    for (uint32_t jj = 0; jj < 8; ++jj)
+                        atomicAdd(&hist[bucket_from_group(w, jj, key, lp.level, pb + jj, bp)], 1u);
+                }
+            } else {
+                for (uint32_t jj = 0; jj < dpg; ++jj) {
+                    const uint64_t p = pb + jj;
+                    if (p >= P0 && p < P1) atomicAdd(&hist[bucket_from_group(w, jj, key, lp.level, p, bp)], 1u);
                 }
             }
         }
@@ -261,157 +270,202 @@ __global__ void k_plan(RunParams rp, LevelParams lp) {
 }
 
 // ---------------------------------------------------------------- scatter --
+// Per CTA: a sequence of tiles (chunks blockIdx.x, +gridDim.x, ..., each walked
+// tile by tile in order).  Tile t lands in buffer t&1 by one bulk async copy
+// issued while tile t-1 is processed.  Each warp loads its 32-element rounds
+// into registers and ranks them (ordered shared atomics, block_ops.cuh); the
+// (bucket, warp) counters are scanned into tile-local bases; the elements are
+// written back into the same buffer in bucket-major stable order; then each
+// warp copies whole bucket runs to dst[running[b] + ...] (coalesced stores).
 template <int EB>
-struct ScatterSmem {
-    static constexpr uint32_t T = kTileBytes / EB;  // elements per tile
-    static constexpr uint32_t Q = T / kWarps;       // elements per warp
-    static constexpr uint32_t R = Q / 32;           // rounds per warp
+struct ScatterCfg {
+    static constexpr uint32_t T = 32768 / EB;       // elements per tile (32 KiB)
+    static constexpr uint32_t R = T / (kWarps * 32);  // rounds per warp
+    static constexpr uint32_t BUF = T * EB + 16;
+};
+
+struct ScatterLayout {
+    uint32_t buf0, buf1, draws, C, bst, delta, running, wsum, bar, total;
 };
 
 template <int EB>
-__host__ __device__ inline uint32_t scatter_smem_layout(uint32_t k, uint32_t* o_in, uint32_t* o_stg, uint32_t* o_slotb,
-                                                        uint32_t* o_draws, uint32_t* o_cwb, uint32_t* o_run,
-                                                        uint32_t* o_bst, uint32_t* o_wsum, uint32_t* o_bar) {
-    constexpr uint32_t T = ScatterSmem<EB>::T;
+__host__ __device__ inline ScatterLayout scatter_layout(uint32_t k) {
+    ScatterLayout L;
     uint32_t off = 0;
-    *o_in = off;
-    off += T * EB + 16;
-    *o_stg = off;
-    off += T * EB;
-    *o_run = off;
-    off += k * 8;
-    *o_bst = off;
-    off += (k + 1) * 4;
-    off = (off + 15) & ~15u;
-    *o_wsum = off;
-    off += (kWarps + 1) * 4;
-    off = (off + 15) & ~15u;
-    *o_bar = off;
-    off += 16;
-    *o_slotb = off;
-    off += T * 2;
-    *o_draws = off;
-    off += T * 2;
-    *o_cwb = off;
-    off += k * kWarps * 2;
-    return (off + 15) & ~15u;
+    auto take = [&off](uint32_t bytes) {
+        const uint32_t at = off;
+        off = (off + bytes + 15u) & ~15u;
+        return at;
+    };
+    L.buf0 = take(ScatterCfg<EB>::BUF);
+    L.buf1 = take(ScatterCfg<EB>::BUF);
+    L.draws = take(draw_bytes(ScatterCfg<EB>::T));
+    L.C = take(kWarps * ((k + 1) / 2) * 4);
+    L.bst = take((k + 1) * 4);
+    L.delta = take(k * 8);
+    L.running = take(k * 8);
+    L.wsum = take((kWarps + 1) * 4);
+    L.bar = take(16);
+    L.total = off;
+    return L;
+}
+
+struct TileRef {
+    uint32_t chunk;   // chunk index (>= nchunk: none)
+    uint64_t q0, q1;  // element range
+    uint64_t seg;     // segment index
+};
+
+__device__ __forceinline__ TileRef first_tile(const LevelParams& lp, const RunParams& rp, uint32_t j, uint32_t nchunk) {
+    TileRef t;
+    t.chunk = j;
+    if (j >= nchunk) {
+        t.q0 = t.q1 = 0;
+        t.seg = 0;
+        return t;
+    }
+    const ChunkDesc ch = lp.chunks[j];
+    const SegDesc& sg = lp.segs[ch.seg];
+    t.seg = ch.seg;
+    t.q0 = sg.start + (uint64_t)ch.c * rp.chunk;
+    t.q1 = min(sg.start + sg.len, t.q0 + rp.chunk);
+    return t;
+}
+
+template <int EB>
+__device__ __forceinline__ void issue_tile_load(const TileRef& t, const unsigned char* src, unsigned char* buf,
+                                                uint64_t* bar) {
+    constexpr uint32_t T = ScatterCfg<EB>::T;
+    const uint32_t tid = threadIdx.x;
+    const uint64_t cnt = (t.q1 - t.q0) < (uint64_t)T ? (t.q1 - t.q0) : (uint64_t)T;
+    const uint64_t x0 = t.q0 * EB, x1 = (t.q0 + cnt) * EB;
+    const uint64_t fl = x0 & ~15ull;
+    const uint64_t A = (x0 + 15) & ~15ull, B = x1 & ~15ull;
+    const bool body = B > A;
+    if (tid == 0) {
+        // arrive with the tx count (0 when there is no aligned body)
+        mbar_arrive_expect_tx(bar, body ? (uint32_t)(B - A) : 0u);
+        if (body) bulk_g2s(buf + (A - fl), src + A, (uint32_t)(B - A), bar);
+    }
+    const uint64_t hEnd = body ? A : x1;
+    const uint32_t nh = (uint32_t)((hEnd - x0) >> 2);
+    const uint64_t tBeg = body ? B : x1;
+    const uint32_t nt = (uint32_t)((x1 - tBeg) >> 2);
+    if (tid >= 32 && tid - 32 < nh)
+        *reinterpret_cast<uint32_t*>(buf + (x0 - fl) + 4 * (tid - 32)) =
+            *reinterpret_cast<const uint32_t*>(src + x0 + 4 * (tid - 32));
+    else if (tid >= 64 && tid - 64 < nt)
+        *reinterpret_cast<uint32_t*>(buf + (tBeg - fl) + 4 * (tid - 64)) =
+            *reinterpret_cast<const uint32_t*>(src + tBeg + 4 * (tid - 64));
 }
 
 template <int EB>
 __global__ void __launch_bounds__(kThreads, 2) k_scatter(RunParams rp, LevelParams lp) {
     using E = typename ElemT<EB>::type;
-    constexpr uint32_t T = ScatterSmem<EB>::T, Q = ScatterSmem<EB>::Q, R = ScatterSmem<EB>::R;
+    constexpr uint32_t T = ScatterCfg<EB>::T, R = ScatterCfg<EB>::R;
     extern __shared__ __align__(16) unsigned char sm[];
-    uint32_t o_in, o_stg, o_slotb, o_draws, o_cwb, o_run, o_bst, o_wsum, o_bar;
-    const uint32_t k = rp.k;
-    scatter_smem_layout<EB>(k, &o_in, &o_stg, &o_slotb, &o_draws, &o_cwb, &o_run, &o_bst, &o_wsum, &o_bar);
-    unsigned char* tile_in = sm + o_in;
-    E* staging = reinterpret_cast<E*>(sm + o_stg);
-    uint16_t* slotb = reinterpret_cast<uint16_t*>(sm + o_slotb);
-    uint16_t* draws = reinterpret_cast<uint16_t*>(sm + o_draws);
-    uint16_t* cwb = reinterpret_cast<uint16_t*>(sm + o_cwb);  // [b][w]
-    uint64_t* running = reinterpret_cast<uint64_t*>(sm + o_run);
-    uint32_t* bst = reinterpret_cast<uint32_t*>(sm + o_bst);
-    uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + o_wsum);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + o_bar);
+    const uint32_t k = rp.k, kw = (k + 1) >> 1;
+    const ScatterLayout Ly = scatter_layout<EB>(k);
+    unsigned char* bufs[2] = {sm + Ly.buf0, sm + Ly.buf1};
+    unsigned char* dsm = sm + Ly.draws;
+    uint32_t* C = reinterpret_cast<uint32_t*>(sm + Ly.C);
+    uint32_t* bst = reinterpret_cast<uint32_t*>(sm + Ly.bst);
+    uint64_t* delta = reinterpret_cast<uint64_t*>(sm + Ly.delta);
+    uint64_t* running = reinterpret_cast<uint64_t*>(sm + Ly.running);
+    uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + Ly.wsum);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + Ly.bar);  // bar[0], bar[1]
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const bool ordered = rp.rank_ordered != 0;
+    const uint32_t nchunk = lp.ctr->nchunk;
+    if (blockIdx.x >= nchunk) return;
     if (tid == 0) {
-        mbar_init(bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
-    uint32_t phase = 0;
-    const uint32_t nchunk = lp.ctr->nchunk;
     const unsigned char* __restrict__ src = lp.src;
     E* __restrict__ dst = reinterpret_cast<E*>(lp.dst);
+    uint32_t ph[2] = {0u, 0u};
 
-    for (uint32_t j = blockIdx.x; j < nchunk; j += gridDim.x) {
-        const ChunkDesc ch = lp.chunks[j];
-        const SegDesc sg = lp.segs[ch.seg];
+    TileRef cur = first_tile(lp, rp, blockIdx.x, nchunk);
+    issue_tile_load<EB>(cur, src, bufs[0], &bar[0]);
+    uint32_t it = 0;
+    bool new_chunk = true;
+    if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->scattered_hbm[lp.level], (unsigned long long)(cur.q1 - cur.q0));
+    while (cur.chunk < nchunk) {
+        const uint32_t cnt = (uint32_t)((cur.q1 - cur.q0) < (uint64_t)T ? (cur.q1 - cur.q0) : (uint64_t)T);
+        // ---- the next tile of this CTA's sequence, prefetched into the other buffer
+        TileRef nxt = cur;
+        nxt.q0 = cur.q0 + cnt;
+        const bool next_chunk = nxt.q0 >= cur.q1;
+        if (next_chunk) nxt = first_tile(lp, rp, cur.chunk + gridDim.x, nchunk);
+        if (nxt.chunk < nchunk) {
+            fence_proxy_async();
+            issue_tile_load<EB>(nxt, src, bufs[(it + 1) & 1], &bar[(it + 1) & 1]);
+            if (next_chunk && tid == 0)
+                atomicAdd((unsigned long long*)&rp.hdr->scattered_hbm[lp.level], (unsigned long long)(nxt.q1 - nxt.q0));
+        }
+        const SegDesc sg = lp.segs[cur.seg];
         const PhiloxKey key = make_key(sg.key);
-        const uint64_t c0 = sg.start + (uint64_t)ch.c * rp.chunk;
-        const uint64_t c1 = min(sg.start + sg.len, c0 + rp.chunk);
-        if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->scattered_hbm[lp.level], (unsigned long long)(c1 - c0));
-        {
+        if (new_chunk) {
+            const ChunkDesc ch = lp.chunks[cur.chunk];
             const uint64_t base0 = lp.prefix[sg.cbase];
             for (uint32_t b = tid; b < k; b += kThreads)
                 running[b] = sg.start + lp.prefix[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] - base0;
         }
-        for (uint64_t q0 = c0; q0 < c1; q0 += T) {
-            const uint32_t cnt = (uint32_t)((c1 - q0) < (uint64_t)T ? (c1 - q0) : (uint64_t)T);
-            const uint64_t q1 = q0 + cnt;
-            // ---- 1. load the tile: aligned body by one bulk copy, head/tail by words
-            const uint64_t x0 = q0 * EB, x1 = q1 * EB;
-            const uint64_t fl = x0 & ~15ull;                // smem byte 0 <-> global byte fl
-            const uint64_t A = (x0 + 15) & ~15ull, B = x1 & ~15ull;
-            const bool body = B > A;
-            if (body && tid == 0) {
-                fence_proxy_async();
-                mbar_arrive_expect_tx(bar, (uint32_t)(B - A));
-                bulk_g2s(tile_in + (A - fl), src + A, (uint32_t)(B - A), bar);
-            }
-            {
-                // head bytes [x0, min(A, x1)) and tail bytes [max(B, A), x1) as 4-byte words
-                const uint64_t hEnd = body ? A : x1;
-                const uint32_t nh = (uint32_t)((hEnd - x0) >> 2);
-                const uint64_t tBeg = body ? B : x1;
-                const uint32_t nt = (uint32_t)((x1 - tBeg) >> 2);
-                if (tid < nh)
-                    *reinterpret_cast<uint32_t*>(tile_in + (x0 - fl) + 4 * tid) =
-                        *reinterpret_cast<const uint32_t*>(src + x0 + 4 * tid);
-                else if (tid >= 32 && tid - 32 < nt)
-                    *reinterpret_cast<uint32_t*>(tile_in + (tBeg - fl) + 4 * (tid - 32)) =
-                        *reinterpret_cast<const uint32_t*>(src + tBeg + 4 * (tid - 32));
-            }
-            // ---- 2. draws (overlaps the bulk load), zero the per-warp counters
-            draws_to_smem(draws, q0 - sg.origin, cnt, key, lp.level, rp.bp);
-            for (uint32_t i = tid; i < k * kWarps; i += kThreads) cwb[i] = 0;
-            __syncthreads();
-            // ---- 3. stable rank: warp w owns [w*Q, (w+1)*Q), rounds of 32 in order
-            uint32_t rk[R];
+        // ---- draws of the tile's positions, zero the counters
+        const DrawView dv = draws_to_smem<kThreads>(dsm, cur.q0 - sg.origin, cnt, key, lp.level, rp.bp);
+        for (uint32_t i = tid; i < kWarps * kw; i += kThreads) C[i] = 0;
+        unsigned char* buf = bufs[it & 1];
+        mbar_wait(&bar[it & 1], ph[it & 1]);
+        ph[it & 1] ^= 1u;
+        __syncthreads();
+        // ---- load my rounds and rank them
+        const unsigned char* tin = buf + ((cur.q0 * EB) & 15u);
+        E v[R];
+        uint32_t rk[R];
+        uint32_t* Cw = C + warp * kw;
 #pragma unroll
-            for (uint32_t r = 0; r < R; ++r) {
-                const uint32_t e = warp * Q + r * 32 + lane;
-                const bool valid = e < cnt;
-                const uint32_t b = valid ? draws[e] : 0xFFFFu;
-                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
-                const uint32_t old = valid ? cwb[b * kWarps + warp] : 0u;
-                __syncwarp();
-                if (valid && lane == (uint32_t)(__ffs(peers) - 1)) cwb[b * kWarps + warp] = (uint16_t)(old + __popc(peers));
-                __syncwarp();
-                rk[r] = old + __popc(peers & lanemask_lt());
+        for (uint32_t r = 0; r < R; ++r) {
+            const uint32_t e = warp * (T / kWarps) + r * 32 + lane;
+            const bool valid = e < cnt;
+            uint32_t b = 0;
+            if (valid) {
+                v[r] = *reinterpret_cast<const E*>(tin + (size_t)e * EB);
+                b = dv.at(e);
             }
-            __syncthreads();
-            // ---- 4. exclusive scan over (bucket, warp): tile-local bases
-            block_exclusive_scan(cwb, k * kWarps, wsum);
-            for (uint32_t b = tid; b < k; b += kThreads) bst[b] = cwb[b * kWarps];
-            if (tid == 0) bst[k] = cnt;
-            if (body) mbar_wait(bar, phase);
-            __syncthreads();
-            if (body) phase ^= 1u;
-            // ---- 5. reorder into staging (bucket-major, stable)
-            const unsigned char* tin = tile_in + (x0 - fl);
-#pragma unroll
-            for (uint32_t r = 0; r < R; ++r) {
-                const uint32_t e = warp * Q + r * 32 + lane;
-                if (e < cnt) {
-                    const uint32_t b = draws[e];
-                    const uint32_t slot = cwb[b * kWarps + warp] + rk[r];
-                    staging[slot] = *reinterpret_cast<const E*>(tin + (size_t)e * EB);
-                    slotb[slot] = (uint16_t)b;
-                }
-            }
-            __syncthreads();
-            // ---- 6. write the bucket runs
-            for (uint32_t s = tid; s < cnt; s += kThreads) {
-                const uint32_t b = slotb[s];
-                dst[running[b] + (s - bst[b])] = staging[s];
-            }
-            __syncthreads();
-            for (uint32_t b = tid; b < k; b += kThreads) running[b] += bst[b + 1] - bst[b];
-            __syncthreads();
+            const uint32_t rank = warp_rank(Cw, b, valid, ordered);
+            rk[r] = valid ? ((b << 16) | rank) : 0xFFFFFFFFu;
         }
+        __syncthreads();
+        scan_counters<kThreads>(C, kWarps, k, bst, wsum);
+        // ---- stable bucket-major placement, in place
+        E* stage = reinterpret_cast<E*>(buf);
+#pragma unroll
+        for (uint32_t r = 0; r < R; ++r) {
+            if (rk[r] != 0xFFFFFFFFu) {
+                const uint32_t b = rk[r] >> 16;
+                const uint32_t base = (Cw[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu;
+                stage[base + (rk[r] & 0xFFFFu)] = v[r];
+            }
+        }
+        for (uint32_t b = tid; b < k; b += kThreads) {
+            delta[b] = running[b] - bst[b];
+            running[b] += bst[b + 1] - bst[b];
+        }
+        __syncthreads();
+        // ---- copy the bucket runs out: warp w takes buckets w, w+16, ...
+        for (uint32_t b = warp; b < k; b += kWarps) {
+            const uint32_t s0 = bst[b], s1 = bst[b + 1];
+            E* d = dst + delta[b];
+            for (uint32_t s = s0 + lane; s < s1; s += 32) d[s] = stage[s];
+        }
+        __syncthreads();
+        new_chunk = next_chunk;
+        cur = nxt;
+        ++it;
     }
 }
 
@@ -443,11 +497,10 @@ cudaError_t launch_plan(const RunParams& rp, const LevelParams& lp, cudaStream_t
 }
 
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k) {
-    uint32_t a, b, c, d, e, f, g, h, i;
     switch (eb) {
-    case 4: return scatter_smem_layout<4>(k, &a, &b, &c, &d, &e, &f, &g, &h, &i);
-    case 8: return scatter_smem_layout<8>(k, &a, &b, &c, &d, &e, &f, &g, &h, &i);
-    default: return scatter_smem_layout<16>(k, &a, &b, &c, &d, &e, &f, &g, &h, &i);
+    case 4: return scatter_layout<4>(k).total;
+    case 8: return scatter_layout<8>(k).total;
+    default: return scatter_layout<16>(k).total;
     }
 }
 

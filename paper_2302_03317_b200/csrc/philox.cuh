@@ -6,13 +6,18 @@
 //        (x0,x1,x2,x3) <- (hi(M1*x2)^x1^k0, lo(M1*x2), hi(M0*x0)^x3^k1, lo(M0*x0))
 //      with M0 = 0xD2511F53, M1 = 0xCD9E8D57; key bumped by the Weyl
 //      constants (0x9E3779B9, 0xBB67AE85) before rounds 2..10.
-//   D4 bucket draw at (level l, problem-relative position p): 16-bit lane
-//      p&7 of Philox(K, (p>>3, l, SC=1)), Lemire with threshold 2^16 mod k;
-//      retries from Philox(K, (p, l | a<<8, SC_RETRY=3)).w0.
-//   D5 FY draw at (position P, bound s): 32-bit word P&3 of
-//      Philox(K, (P>>2, 0, FY=2)), Lemire with threshold 2^32 mod s;
-//      retries from Philox(K, (P, a, FY_RETRY=4)).w0.
-//   Paper: Lemire bounded integers P:99-100; FY partner draw Fig. 1 P:109.
+//   D4 bucket draw at (level l, problem-relative position p):
+//      k a power of two <= 256 ("narrow"): 8-bit lane p&15 of
+//        Philox(K, (p>>4, l, SC=1)) shifted right by 8 - log2 k;
+//      otherwise ("wide"): 16-bit lane p&7 of Philox(K, (p>>3, l, SC=1)),
+//        Lemire with threshold 2^16 mod k, retries from
+//        Philox(K, (p, l | a<<8, SC_RETRY=3)).w0 & 0xFFFF.
+//   D5 FY draw at (position P, bound s):
+//      s <= 2^16: 16-bit lane P&7 of Philox(K, (P>>3, 0, FY16=2)), Lemire16,
+//        retries from Philox(K, (P, a, FY16_RETRY=4)).w0 & 0xFFFF;
+//      s >  2^16: word P&3 of Philox(K, (P>>2, 0, FY32=5)), Lemire32,
+//        retries from Philox(K, (P, a, FY32_RETRY=6)).w0.
+//   Fig. 1: partner = gen_index(rng, i+1), i.e. s = i + 1.
 #pragma once
 #include <cstdint>
 
@@ -41,95 +46,119 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, PhiloxKey key) {
     return c;
 }
 
-enum : uint32_t { TAG_SC = 1u, TAG_FY = 2u, TAG_SC_RETRY = 3u, TAG_FY_RETRY = 4u };
+enum : uint32_t {
+    TAG_SC = 1u,
+    TAG_FY16 = 2u,
+    TAG_SC_RETRY = 3u,
+    TAG_FY16_RETRY = 4u,
+    TAG_FY32 = 5u,
+    TAG_FY32_RETRY = 6u
+};
 
-// Bucket-draw parameters for one k (power of two or general).
+// Bucket-draw parameters for one k.
 struct BucketParams {
     uint32_t k;
-    uint32_t t;      // 2^16 mod k (0 for powers of two: no rejection)
-    uint32_t shift;  // 16 - log2(k) when k is a power of two, else 0xFFFFFFFF
+    uint32_t narrow;  // 1: power of two <= 256 -> 16 draws per call, 8-bit lanes
+    uint32_t shift;   // narrow: 8 - log2 k; wide power of two: 16 - log2 k; else 0xFFFFFFFF
+    uint32_t t;       // wide, general k: 2^16 mod k
 };
 
 __host__ __device__ inline BucketParams make_bucket_params(uint32_t k) {
     BucketParams bp;
     bp.k = k;
     bp.t = 65536u % k;
-    bp.shift = 0xFFFFFFFFu;
-    if ((k & (k - 1)) == 0) {
-        uint32_t b = 0;
-        while ((1u << b) < k) ++b;
-        bp.shift = 16u - b;
-    }
+    uint32_t b = 0;
+    while ((1u << b) < k) ++b;
+    const bool pow2 = (k & (k - 1)) == 0;
+    bp.narrow = (pow2 && k <= 256u) ? 1u : 0u;
+    bp.shift = pow2 ? (bp.narrow ? 8u - b : 16u - b) : 0xFFFFFFFFu;
     return bp;
 }
 
-// The 8 primary 16-bit lanes of group g at level l.
+__host__ __device__ inline uint32_t draws_per_group(const BucketParams& bp) { return bp.narrow ? 16u : 8u; }
+
+// The 128 bits of group g at level l (both lane widths use this counter).
 __device__ __forceinline__ uint4 bucket_group_words(PhiloxKey key, uint32_t level, uint64_t g) {
     return philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), level, TAG_SC), key);
 }
 
-// Slow path of D4: retry stream for a rejected position.
-static __device__ __noinline__ uint32_t bucket_retry(PhiloxKey key, uint32_t level, uint64_t p, BucketParams bp) {
+// Slow path of D4 (wide, non-power-of-two k): retry stream.
+static __device__ __noinline__ uint32_t bucket_retry(PhiloxKey key, uint32_t level, uint64_t p, uint32_t k,
+                                                     uint32_t t) {
     for (uint32_t a = 1;; ++a) {
         uint4 w = philox4x32_10(make_uint4((uint32_t)p, (uint32_t)(p >> 32), level | (a << 8), TAG_SC_RETRY), key);
-        uint32_t m = (w.x & 0xFFFFu) * bp.k;
-        if ((m & 0xFFFFu) >= bp.t) return m >> 16;
+        uint32_t m = (w.x & 0xFFFFu) * k;
+        if ((m & 0xFFFFu) >= t) return m >> 16;
     }
 }
 
-// Map one primary 16-bit lane v (of position p) to a bucket.
-__device__ __forceinline__ uint32_t bucket_from_lane(uint32_t v, PhiloxKey key, uint32_t level, uint64_t p,
-                                                     BucketParams bp) {
-    if (bp.shift != 0xFFFFFFFFu) return v >> bp.shift;
-    uint32_t m = v * bp.k;
-    if ((m & 0xFFFFu) >= bp.t) return m >> 16;
-    return bucket_retry(key, level, p, bp);
+__device__ __forceinline__ uint32_t word_of(uint4 w, uint32_t i) {
+    return (i < 2) ? ((i == 0) ? w.x : w.y) : ((i == 2) ? w.z : w.w);
 }
 
+__device__ __forceinline__ uint32_t lane8(uint4 w, uint32_t j) { return (word_of(w, j >> 2) >> ((j & 3u) * 8u)) & 0xFFu; }
 __device__ __forceinline__ uint32_t lane16(uint4 w, uint32_t j) {
-    uint32_t word = (j < 4) ? ((j < 2) ? w.x : w.y) : ((j < 6) ? w.z : w.w);
-    return (word >> ((j & 1u) * 16u)) & 0xFFFFu;
+    return (word_of(w, j >> 1) >> ((j & 1u) * 16u)) & 0xFFFFu;
 }
 
-// D4 for a single position (used off the hot loops).
-__device__ __forceinline__ uint32_t bucket_draw(PhiloxKey key, uint32_t level, uint64_t p, BucketParams bp) {
-    uint4 w = bucket_group_words(key, level, p >> 3);
-    return bucket_from_lane(lane16(w, (uint32_t)(p & 7u)), key, level, p, bp);
+// Bucket of lane j of group g (position p = g*dpg + j).
+__device__ __forceinline__ uint32_t bucket_from_group(uint4 w, uint32_t j, PhiloxKey key, uint32_t level, uint64_t p,
+                                                      const BucketParams& bp) {
+    if (bp.narrow) return lane8(w, j) >> bp.shift;
+    const uint32_t v = lane16(w, j);
+    if (bp.shift != 0xFFFFFFFFu) return v >> bp.shift;
+    const uint32_t m = v * bp.k;
+    if ((m & 0xFFFFu) >= bp.t) return m >> 16;
+    return bucket_retry(key, level, p, bp.k, bp.t);
 }
 
-// D5 slow path.
-static __device__ __noinline__ uint32_t fy_retry(PhiloxKey key, uint64_t P, uint32_t s) {
-    const uint32_t t = (uint32_t)(0x100000000ull % s);
+// D4 for a single position (off the hot loops).
+__device__ __forceinline__ uint32_t bucket_draw(PhiloxKey key, uint32_t level, uint64_t p, const BucketParams& bp) {
+    const uint32_t sh = bp.narrow ? 4u : 3u;
+    const uint4 w = bucket_group_words(key, level, p >> sh);
+    return bucket_from_group(w, (uint32_t)(p & ((1u << sh) - 1u)), key, level, p, bp);
+}
+
+// ---------------------------------------------------------------- D5 ----
+__device__ __forceinline__ uint4 fy16_group_words(PhiloxKey key, uint64_t g) {
+    return philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, TAG_FY16), key);
+}
+
+static __device__ __noinline__ uint32_t fy16_retry(PhiloxKey key, uint64_t P, uint32_t s) {
+    const uint32_t t = 65536u % s;
     for (uint32_t a = 1;; ++a) {
-        uint4 w = philox4x32_10(make_uint4((uint32_t)P, (uint32_t)(P >> 32), a, TAG_FY_RETRY), key);
-        uint64_t M = (uint64_t)w.x * s;
-        if ((uint32_t)M >= t) return (uint32_t)(M >> 32);
+        uint4 w = philox4x32_10(make_uint4((uint32_t)P, (uint32_t)(P >> 32), a, TAG_FY16_RETRY), key);
+        const uint32_t m = (w.x & 0xFFFFu) * s;
+        if ((m & 0xFFFFu) >= t) return m >> 16;
     }
 }
 
-// Lemire on one primary word w of position P; the 2^32 mod s threshold is
-// only evaluated when the cheap pre-check lo < s fails to rule rejection out.
-__device__ __forceinline__ uint32_t fy_from_word(uint32_t w, PhiloxKey key, uint64_t P, uint32_t s) {
-    uint64_t M = (uint64_t)w * s;
-    uint32_t lo = (uint32_t)M;
-    if (lo < s) {
-        const uint32_t t = (uint32_t)(0x100000000ull % s);
-        if (lo < t) return fy_retry(key, P, s);
+// Lemire16 on lane v of position P with bound s <= 2^16; the modulo is only
+// evaluated when the cheap pre-check (low part < s) cannot rule rejection out.
+__device__ __forceinline__ uint32_t fy16_from_lane(uint32_t v, PhiloxKey key, uint64_t P, uint32_t s) {
+    const uint32_t m = v * s;
+    const uint32_t lo = m & 0xFFFFu;
+    if (lo < s && lo < 65536u % s) return fy16_retry(key, P, s);
+    return m >> 16;
+}
+
+static __device__ __noinline__ uint32_t fy32_draw(PhiloxKey key, uint64_t P, uint32_t s) {
+    const uint32_t t = (uint32_t)(0x100000000ull % s);
+    const uint64_t g = P >> 2;
+    uint4 w = philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, TAG_FY32), key);
+    uint64_t M = (uint64_t)word_of(w, (uint32_t)(P & 3u)) * s;
+    for (uint32_t a = 1; (uint32_t)M < t; ++a) {
+        w = philox4x32_10(make_uint4((uint32_t)P, (uint32_t)(P >> 32), a, TAG_FY32_RETRY), key);
+        M = (uint64_t)w.x * s;
     }
     return (uint32_t)(M >> 32);
 }
 
-__device__ __forceinline__ uint4 fy_group_words(PhiloxKey key, uint64_t g) {
-    return philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, TAG_FY), key);
-}
-
-__device__ __forceinline__ uint32_t word32(uint4 w, uint32_t j) {
-    return (j < 2) ? ((j == 0) ? w.x : w.y) : ((j == 2) ? w.z : w.w);
-}
-
+// D5 for a single step (off the hot loops).
 __device__ __forceinline__ uint32_t fy_draw(PhiloxKey key, uint64_t P, uint32_t s) {
-    uint4 w = fy_group_words(key, P >> 2);
-    return fy_from_word(word32(w, (uint32_t)(P & 3u)), key, P, s);
+    if (s > 65536u) return fy32_draw(key, P, s);
+    const uint4 w = fy16_group_words(key, P >> 3);
+    return fy16_from_lane(lane16(w, (uint32_t)(P & 7u)), key, P, s);
 }
 
 }  // namespace shuf

@@ -6,7 +6,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -20,12 +22,13 @@ struct shuf_plan_s {
     uint64_t n;
     uint32_t eb, k, L;
     uint64_t seed;
-    uint32_t S_fuse, chunk, levels;
+    uint32_t S_fuse, chunk, levels, fin_nbuf;
     ScratchLayout lay;
     // device setup (lazily, first run)
     bool dev_ready;
     int sms;
     int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small;
+    int rank_ordered;
     uint32_t finish_smem, scatter_smem;
     int last_cuda_error;
     uint64_t last_launches;
@@ -37,18 +40,27 @@ static thread_local shuf_status g_last_status = SHUF_OK;
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 // Largest S with finish_smem_bytes(S) <= the opt-in shared-memory limit,
-// capped so that in-smem frontiers (<= S/(L+1) entries) fit kFrontierCap and
-// u16 indices suffice.
-static uint32_t pick_s_fuse(uint32_t eb, uint32_t k, uint32_t L) {
+// capped by the ranking registers (finish_max_elems), u16 tile-local
+// offsets, and in-smem frontiers (<= S/(L+1) entries <= kFrontierCap).
+static uint32_t pick_s_fuse_nbuf(uint32_t eb, uint32_t k, uint32_t L, uint32_t nbuf) {
     uint32_t lo = 1, hi = 65535;
     while (lo < hi) {
         uint32_t mid = (lo + hi + 1) / 2;
-        if (finish_smem_bytes(mid, eb, k) <= kSmemLimit) lo = mid;
+        if (finish_smem_bytes(mid, eb, k, nbuf) <= kSmemLimit) lo = mid;
         else hi = mid - 1;
     }
+    const uint32_t rmax = finish_max_elems(eb, k);
+    if (rmax < lo) lo = rmax;
     uint64_t cap = (uint64_t)kFrontierCap * ((uint64_t)L + 1);
     if (cap < lo) lo = (uint32_t)cap;
     return lo;
+}
+
+static uint32_t pick_s_fuse(uint32_t eb, uint32_t k, uint32_t L, uint32_t* nbuf) {
+    const uint32_t s2 = pick_s_fuse_nbuf(eb, k, L, 2), s1 = pick_s_fuse_nbuf(eb, k, L, 1);
+    // double-buffer the items unless that costs more than 10% of the fusable size
+    *nbuf = (10ull * s2 >= 9ull * s1) ? 2u : 1u;
+    return *nbuf == 2 ? s2 : s1;
 }
 
 // Global levels needed until the largest segment fits S_fuse, with a
@@ -108,7 +120,8 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
         g_last_status = SHUF_ERR_UNSUPPORTED;
         return nullptr;
     }
-    const uint32_t S = pick_s_fuse(elem_bytes, k, L);
+    uint32_t nbuf = 1;
+    const uint32_t S = pick_s_fuse(elem_bytes, k, L, &nbuf);
     if (L > S) {
         g_last_status = SHUF_ERR_UNSUPPORTED;
         return nullptr;
@@ -124,7 +137,8 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     p->L = L;
     p->seed = seed;
     p->S_fuse = S;
-    const uint32_t T = kTileBytes / elem_bytes;
+    p->fin_nbuf = nbuf;
+    const uint32_t T = 32768u / elem_bytes;  // scatter tile (kernels_level.cu ScatterCfg)
     uint64_t C = (n + 16383) / 16384;
     C = align_up(C < T ? T : C, T);
     if (C > 0x40000000ull) C = 0x40000000ull;
@@ -151,13 +165,48 @@ static shuf_status cuda_fail(shuf_plan_s* p, cudaError_t e) {
     return SHUF_ERR_CUDA;
 }
 
+// One-time (per process) check that same-address shared atomics of a warp
+// return in lane order (block_ops.cuh); SHUF_RANK_MODE=match|atomic overrides.
+static int g_rank_ordered = -1;
+static std::mutex g_probe_mu;
+
+static cudaError_t probe_rank_order(int sms, int* ordered) {
+    std::lock_guard<std::mutex> lk(g_probe_mu);
+    if (g_rank_ordered >= 0) {
+        *ordered = g_rank_ordered;
+        return cudaSuccess;
+    }
+    const char* env = std::getenv("SHUF_RANK_MODE");
+    if (env && std::strcmp(env, "match") == 0) {
+        g_rank_ordered = 0;
+    } else if (env && std::strcmp(env, "atomic") == 0) {
+        g_rank_ordered = 1;
+    } else {
+        uint32_t* d = nullptr;
+        cudaError_t e = cudaMalloc(&d, sizeof(uint32_t));
+        if (e) return e;
+        uint32_t h = 0;
+        if (!(e = cudaMemset(d, 0, sizeof(uint32_t))) && !(e = launch_rank_order_probe(sms, d, 0)) &&
+            !(e = cudaDeviceSynchronize()))
+            e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        if (e) return e;
+        g_rank_ordered = (h == 0) ? 1 : 0;
+    }
+    *ordered = g_rank_ordered;
+    return cudaSuccess;
+}
+
+extern "C" int shuf_rank_mode(void) { return g_rank_ordered; }
+
 static cudaError_t device_setup(shuf_plan_s* p) {
     if (p->dev_ready) return cudaSuccess;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e) return e;
     if ((e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-    p->finish_smem = finish_smem_bytes(p->S_fuse, p->eb, p->k);
+    if ((e = probe_rank_order(p->sms, &p->rank_ordered))) return e;
+    p->finish_smem = finish_smem_bytes(p->S_fuse, p->eb, p->k, p->fin_nbuf);
     p->scatter_smem = scatter_smem_bytes(p->eb, p->k);
     if ((e = configure_finish(p->finish_smem))) return e;
     if ((e = configure_scatter(p->scatter_smem))) return e;
@@ -258,6 +307,8 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     rp.run_leaves = run_leaves;
     rp.bp = make_bucket_params(p->k);
     rp.seed = p->seed;
+    rp.rank_ordered = (uint32_t)p->rank_ordered;
+    rp.fin_nbuf = p->fin_nbuf;
     uint64_t launches = 0;
     if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
     const LevelParams lp0 = level_params(p, sc, buf0, 0);
@@ -276,6 +327,7 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         LAUNCH(SHUF_K_PLAN, launch_plan(rp, lp, st, p->grid_small));
         LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
+        if (lv + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
     }
     p->last_launches = launches;
     return SHUF_OK;

@@ -11,7 +11,6 @@ namespace shuf {
 // ----------------------------------------------------------- constants ----
 constexpr int kWarps = 16;                 // warps per CTA in the ranking kernels
 constexpr int kThreads = kWarps * 32;      // 512
-constexpr uint32_t kTileBytes = 16384;     // one scatter tile (T = kTileBytes / eb elements)
 constexpr uint32_t kMaxK = 1024;           // device bucket-count limit
 constexpr uint32_t kScanTile = 4096;       // entries per decoupled-lookback tile
 constexpr uint32_t kSmemLimit = 227 * 1024;
@@ -88,6 +87,8 @@ struct RunParams {
     int run_leaves;
     BucketParams bp;
     uint64_t seed;
+    uint32_t rank_ordered;  // 1: ordered shared atomics verified on this GPU (block_ops.cuh)
+    uint32_t fin_nbuf;      // finish-kernel data buffers (2 = items double-buffered)
 };
 
 struct LevelParams {
@@ -119,7 +120,10 @@ cudaError_t launch_plan(const RunParams& rp, const LevelParams& lp, cudaStream_t
 cudaError_t launch_finish_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
                                    cudaStream_t s, int grid);
-uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k);
+uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t nbuf);
+uint32_t finish_max_elems(uint32_t eb, uint32_t k);
+cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);
 cudaError_t configure_scatter(uint32_t smem);
 cudaError_t configure_finish(uint32_t smem);
