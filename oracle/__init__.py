@@ -126,10 +126,11 @@ def bucket_draw(K: int, level: int, p: int, k: int):
     return int(b), int(rej.value)
 
 
-def fy_draw(K: int, P: int, s: int):
-    """D5 for one FY step; returns (partner, retries)."""
+def fy_draw(K: int, q: int, i: int):
+    """D5 for step i (bound i+1) of the leaf starting at problem position q;
+    returns (partner, retries)."""
     rej = ctypes.c_uint64(0)
-    j = lib().oracle_fy_draw(K, P, s, ctypes.byref(rej))
+    j = lib().oracle_fy_draw(K, q, i, ctypes.byref(rej))
     return int(j), int(rej.value)
 
 
@@ -139,11 +140,12 @@ def bucket_draws(K: int, level: int, p0: int, count: int, k: int) -> np.ndarray:
     return out
 
 
-def fy_draws(K: int, P, s) -> np.ndarray:
-    P = np.ascontiguousarray(P, dtype=np.uint64)
-    s = np.ascontiguousarray(s, dtype=np.uint32)
-    out = np.zeros(P.shape[0], dtype=np.uint32)
-    lib().oracle_fy_draws(K, _ptr(P), _ptr(s), P.shape[0], _ptr(out))
+def fy_draws(K: int, q, i) -> np.ndarray:
+    """D5 for arrays of (leaf start q, step i)."""
+    q = np.ascontiguousarray(np.broadcast_to(np.asarray(q, dtype=np.uint64), np.shape(i)))
+    i = np.ascontiguousarray(i, dtype=np.uint32)
+    out = np.zeros(i.shape[0], dtype=np.uint32)
+    lib().oracle_fy_draws(K, _ptr(q), _ptr(i), i.shape[0], _ptr(out))
     return out
 
 

@@ -18,7 +18,7 @@
  *                              8-bit lanes (16 draws per Philox call) for
  *                              power-of-two k <= 256, 16-bit lanes otherwise
  *   D5 Fisher-Yates draw .... Fig. 1: gen_index(rng, i+1),
- *                              "partner from [0..i]"
+ *                              "partner from [0..i]", keyed by (leaf, step)
  *   D6 recursion ............ ScatterShuffle, IpSc "groups X by A
  *                              ... with some permutation pi that sorts A"
  *                               with pi chosen stable; recursion and
@@ -166,54 +166,48 @@ uint32_t oracle_bucket_draw(uint64_t K, uint32_t level, uint64_t p, uint32_t k, 
 }
 
 /* ---------------------------------------------------------------- D5 ---- */
-/* D5: Fisher-Yates partner for the step at problem-relative position P with
- * bound s = i+1 (Fig. 1: gen_index(rng, i+1), "partner from [0..i]").
- * s <= 2^16: 16-bit lane P&7 of Philox(K, (P>>3, 0, FY16)), Lemire16, retries
- *   from Philox(K, (P, a, FY16_RETRY)).w0 & 0xFFFF.
- * s >  2^16: 32-bit word P&3 of Philox(K, (P>>2, 0, FY32)), Lemire32, retries
- *   from Philox(K, (P, a, FY32_RETRY)).w0. */
-uint32_t oracle_fy_draw(uint64_t K, uint64_t P, uint32_t s, uint64_t *rejections)
+/* D5: Fisher-Yates partner for step i (bound s = i+1) of the leaf whose first
+ * element is problem-relative position q -- keyed by (seed, leaf id, step)
+ * (Fig. 1: gen_index(rng, i+1), "partner from [0..i]").
+ * s <= 2^16: 16-bit lane i&7 of Philox(K, (q, i>>3, FY16)), Lemire16.
+ * s >  2^16: 32-bit word i&3 of Philox(K, (q, i>>2, FY32)), Lemire32.
+ * Retry a >= 1: Philox(K, (q, i, TAG_RETRY | a<<8)).w0 (low 16 bits for
+ * 16-bit lanes), TAG_RETRY = FY16_RETRY or FY32_RETRY. */
+uint32_t oracle_fy_draw(uint64_t K, uint64_t q, uint32_t i, uint64_t *rejections)
 {
     uint32_t key[2], ctr[4], w[4], out;
+    const uint32_t s = i + 1u;
     key_words(K, key);
+    ctr[0] = (uint32_t)q;
+    ctr[1] = (uint32_t)(q >> 32);
     if (s <= 65536u) {
-        uint64_t g = P >> 3;
-        ctr[0] = (uint32_t)g;
-        ctr[1] = (uint32_t)(g >> 32);
-        ctr[2] = 0;
+        ctr[2] = i >> 3;
         ctr[3] = TAG_FY16;
         oracle_philox4x32_10(ctr, key, w);
-        uint32_t j = (uint32_t)(P & 7u);
+        uint32_t j = i & 7u;
         uint32_t v = (w[j >> 1] >> (16u * (j & 1u))) & 0xFFFFu;
         if (oracle_lemire16_accept(v, s, &out))
             return out;
         for (uint32_t a = 1;; a++) {
             if (rejections)
                 (*rejections)++;
-            ctr[0] = (uint32_t)P;
-            ctr[1] = (uint32_t)(P >> 32);
-            ctr[2] = a;
-            ctr[3] = TAG_FY16_RETRY;
+            ctr[2] = i;
+            ctr[3] = TAG_FY16_RETRY | (a << 8);
             oracle_philox4x32_10(ctr, key, w);
             if (oracle_lemire16_accept(w[0] & 0xFFFFu, s, &out))
                 return out;
         }
     }
-    uint64_t g = P >> 2;
-    ctr[0] = (uint32_t)g;
-    ctr[1] = (uint32_t)(g >> 32);
-    ctr[2] = 0;
+    ctr[2] = i >> 2;
     ctr[3] = TAG_FY32;
     oracle_philox4x32_10(ctr, key, w);
-    if (oracle_lemire32_accept(w[P & 3u], s, &out))
+    if (oracle_lemire32_accept(w[i & 3u], s, &out))
         return out;
     for (uint32_t a = 1;; a++) {
         if (rejections)
             (*rejections)++;
-        ctr[0] = (uint32_t)P;
-        ctr[1] = (uint32_t)(P >> 32);
-        ctr[2] = a;
-        ctr[3] = TAG_FY32_RETRY;
+        ctr[2] = i;
+        ctr[3] = TAG_FY32_RETRY | (a << 8);
         oracle_philox4x32_10(ctr, key, w);
         if (oracle_lemire32_accept(w[0], s, &out))
             return out;
@@ -227,10 +221,10 @@ void oracle_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count
         out[i] = oracle_bucket_draw(K, level, p0 + i, k, NULL);
 }
 
-void oracle_fy_draws(uint64_t K, const uint64_t *P, const uint32_t *s, uint64_t count, uint32_t *out)
+void oracle_fy_draws(uint64_t K, const uint64_t *q, const uint32_t *i, uint64_t count, uint32_t *out)
 {
-    for (uint64_t i = 0; i < count; i++)
-        out[i] = oracle_fy_draw(K, P[i], s[i], NULL);
+    for (uint64_t x = 0; x < count; x++)
+        out[x] = oracle_fy_draw(K, q[x], i[x], NULL);
 }
 
 /* --------------------------------------------------------- elements ---- */
@@ -276,12 +270,13 @@ typedef struct {
     oracle_stats *st;
 } ctx_t;
 
-/* Fig. 1: for i = m-1 down to 1: swap(A[q+i], A[q + gen_index(i+1)]).       */
+/* Fig. 1: for i = m-1 down to 1: swap(A[q+i], A[q + gen_index(i+1)]),
+ * the draw keyed by (leaf id q, step i) (D5).                                */
 static void fy_leaf(ctx_t *c, uint64_t q, uint64_t m)
 {
     uint64_t *rej = c->st ? &c->st->fy_rejections : NULL;
     for (uint64_t i = m; i-- > 1;) {
-        uint32_t j = oracle_fy_draw(c->K, q + i, (uint32_t)(i + 1), rej);
+        uint32_t j = oracle_fy_draw(c->K, q, (uint32_t)i, rej);
         elem_swap(c->A + (q + i) * c->eb, c->A + (q + j) * c->eb, c->eb);
     }
 }

@@ -24,9 +24,9 @@ uint64_t oracle_problem_key(uint64_t seed, uint64_t s);
 int oracle_lemire16_accept(uint32_t v, uint32_t s, uint32_t *out);
 int oracle_lemire32_accept(uint32_t w, uint32_t s, uint32_t *out);
 uint32_t oracle_bucket_draw(uint64_t K, uint32_t level, uint64_t p, uint32_t k, uint64_t *rejections);
-uint32_t oracle_fy_draw(uint64_t K, uint64_t P, uint32_t s, uint64_t *rejections);
+uint32_t oracle_fy_draw(uint64_t K, uint64_t q, uint32_t i, uint64_t *rejections);
 void oracle_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count, uint32_t k, uint32_t *out);
-void oracle_fy_draws(uint64_t K, const uint64_t *P, const uint32_t *s, uint64_t count, uint32_t *out);
+void oracle_fy_draws(uint64_t K, const uint64_t *q, const uint32_t *i, uint64_t count, uint32_t *out);
 void oracle_fy_with_draws(void *data, uint64_t m, uint32_t eb, const uint32_t *j);
 int oracle_shuffle(void *data, uint64_t n, uint32_t eb, uint32_t k, uint32_t L, uint64_t seed,
                    uint32_t max_levels, int run_leaves, oracle_stats *st);

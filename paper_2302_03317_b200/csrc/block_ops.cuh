@@ -131,22 +131,27 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* Cw, uint32_t b, bool val
 // C holds nw packed-u16 counter tables of k entries (table w at C + w*kw,
 // kw = ceil(k/2) words).  Replace every count by its exclusive prefix in
 // (bucket, warp) order and write bucket starts to bst[0..k] (bst[k] = total).
-// Requires kw <= NT.  All NT threads call.
+// Each thread owns a contiguous run of words.  All NT threads call.
 template <int NT>
 __device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum) {
-    const uint32_t x = threadIdx.x;  // word = buckets 2x, 2x+1
     const uint32_t kw = (k + 1) >> 1;
-    uint32_t t0 = 0, t1 = 0;
-    if (x < kw) {
+    const uint32_t per = (kw + NT - 1) / NT;
+    const uint32_t x0 = threadIdx.x * per, x1 = min(kw, x0 + per);
+    uint32_t mine = 0;
+    for (uint32_t x = x0; x < x1; ++x)
+        for (uint32_t w = 0; w < nw; ++w) {
+            const uint32_t c = C[w * kw + x];
+            mine += (c & 0xFFFFu) + (c >> 16);
+        }
+    uint32_t total;
+    uint32_t run = block_exclusive_sum<NT>(mine, wsum, &total);
+    for (uint32_t x = x0; x < x1; ++x) {
+        uint32_t t0 = 0, t1 = 0;
         for (uint32_t w = 0; w < nw; ++w) {
             const uint32_t c = C[w * kw + x];
             t0 += c & 0xFFFFu;
             t1 += c >> 16;
         }
-    }
-    uint32_t total;
-    const uint32_t run = block_exclusive_sum<NT>(t0 + t1, wsum, &total);
-    if (x < kw) {
         bst[2 * x] = run;
         if (2 * x + 1 < k) bst[2 * x + 1] = run + t0;
         uint32_t r0 = run, r1 = run + t0;
@@ -156,8 +161,9 @@ __device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t
             r0 += c & 0xFFFFu;
             r1 += c >> 16;
         }
+        run += t0 + t1;
     }
-    if (x == 0) bst[k] = total;
+    if (threadIdx.x == 0) bst[k] = total;
     __syncthreads();
 }
 

@@ -1,67 +1,36 @@
 // Fused finish: every segment of at most S_fuse elements is finished by one
 // CTA in a single HBM round trip -- all of its remaining scatter levels run
 // in shared memory (same draws, same stable order as the HBM levels), every
-// leaf (<= L elements) is Fisher-Yates'd in place (Fig. 1), and
-// the finished segment goes back to ptr with one bulk async store.
+// leaf (<= L elements) is Fisher-Yates'd (Fig. 1), and the
+// finished segment goes back to ptr with one bulk async store.
 //
-// Items are pipelined: while item t is processed in buffer t&1, item t+1 is
-// already being loaded into the other buffer by the bulk-copy engine.
+// One CTA of 1024 threads per SM, two data buffers in shared memory: the
+// item arrives in IN (bulk async copy), the stable scatter writes it to OUT,
+// and as soon as IN has been consumed the next item's copy is issued, so the
+// load overlaps this item's Fisher-Yates phase and store.  Every
+// shared-memory pointer is derived from the one extern array `fsm`, so all
+// accesses compile to LDS/STS/ATOMS.
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "block_ops.cuh"
 #include "shuf_internal.cuh"
 
 namespace shuf {
 
-constexpr int kFinThreads = 1024;
-constexpr int kFinWarps = kFinThreads / 32;
+extern __shared__ __align__(16) unsigned char fsm[];
 
-template <int EB> struct FinCfg;
-template <> struct FinCfg<4> { static constexpr uint32_t RMAX = 18; };
-template <> struct FinCfg<8> { static constexpr uint32_t RMAX = 12; };
-template <> struct FinCfg<16> { static constexpr uint32_t RMAX = 6; };
+constexpr int NTF = 1024;                       // threads per finish CTA
+constexpr uint32_t kUnit = kFinishBucketGroup;  // children per work unit
 
+// Warps that rank: all 32 while their per-warp counter tables stay small
+// (Wr * k/2 words <= 4096), fewer for large k.
 __host__ __device__ inline uint32_t finish_rank_warps(uint32_t k) {
-    uint32_t w = 16384u / k;
-    return w > (uint32_t)kFinWarps ? (uint32_t)kFinWarps : (w < 1 ? 1u : w);
+    const uint32_t kw = (k + 1) / 2 > 0 ? (k + 1) / 2 : 1;
+    const uint32_t w = 4096u / kw;
+    return w > 32u ? 32u : (w < 1 ? 1u : w);
 }
-
-__host__ __device__ inline uint32_t finish_rmax(uint32_t eb) {
-    return eb == 4 ? FinCfg<4>::RMAX : (eb == 8 ? FinCfg<8>::RMAX : FinCfg<16>::RMAX);
-}
-
-struct FinishLayout {
-    uint32_t buf[2], draws, C, bst, wsum, front0, front1, misc, bar, ctl, total;
-};
-
-__host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, uint32_t k, uint32_t nbuf) {
-    FinishLayout f;
-    uint32_t off = 0;
-    auto take = [&off](uint32_t bytes) {
-        const uint32_t at = off;
-        off = (off + bytes + 15u) & ~15u;
-        return at;
-    };
-    f.buf[0] = take(S * eb + 32);
-    f.buf[1] = nbuf > 1 ? take(S * eb + 32) : f.buf[0];
-    f.draws = take(draw_bytes(S));
-    f.C = take(finish_rank_warps(k) * ((k + 1) / 2) * 4);
-    f.bst = take((k + 1) * 4);
-    f.wsum = take((kFinWarps + 1) * 4);
-    f.front0 = take(kFrontierCap * 4);
-    f.front1 = take(kFrontierCap * 4);
-    f.misc = take(64);
-    f.bar = take(16);
-    f.ctl = take(256);
-    f.total = off;
-    return f;
-}
-
-uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t nbuf) {
-    return finish_layout(S_fuse, eb, k, nbuf).total;
-}
-
-uint32_t finish_max_elems(uint32_t eb, uint32_t k) { return finish_rmax(eb) * finish_rank_warps(k) * 32u; }
 
 struct Item {
     uint64_t start;
@@ -71,31 +40,68 @@ struct Item {
     uint64_t key;
 };
 
-// Per-CTA control block in shared memory: the current and next item and the
-// iterator state are kept here (written by thread 0) so that the 1024
-// threads' registers stay free for the ranking rounds.
+// Per-CTA control block (shared memory offset 0): iterator state and the
+// current/next item, written by warp 0 and read by everyone.
 struct FinCtl {
     Item items[2];
     uint32_t have[2];
-    uint64_t u, units;   // iterator: unit cursor / count
-    uint32_t b, bend;    // iterator: bucket cursor within the unit
-    uint32_t phase[2];   // mbarrier phase per buffer
+    uint32_t phase;      // mbarrier phase of the IN buffer
+    uint32_t nfront;     // children queued for the next in-smem level
+    uint64_t u, units;   // iterator: work-unit cursor / count
+    uint32_t b, bend;    // iterator: child cursor within the unit
+    uint64_t seg_start, seg_origin, seg_key;
+    uint64_t ub[kUnit + 1];  // unit child boundaries (relative to seg_start)
+    unsigned long long st_finished, st_smem[32];
 };
 
-struct FinCtx {
-    unsigned char* sm;
+struct FinishLayout {
+    uint32_t in, out, draws, C, bst, wsum, front0, front1, bar, total;
+};
+
+__host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, uint32_t k) {
     FinishLayout f;
-    __device__ __forceinline__ unsigned char* buf(uint32_t i) const { return sm + f.buf[i]; }
-    __device__ __forceinline__ unsigned char* draws() const { return sm + f.draws; }
-    __device__ __forceinline__ uint32_t* C() const { return reinterpret_cast<uint32_t*>(sm + f.C); }
-    __device__ __forceinline__ uint32_t* bst() const { return reinterpret_cast<uint32_t*>(sm + f.bst); }
-    __device__ __forceinline__ uint32_t* wsum() const { return reinterpret_cast<uint32_t*>(sm + f.wsum); }
+    uint32_t off = 0;
+    auto take = [&off](uint32_t bytes) {
+        const uint32_t at = off;
+        off = (off + bytes + 15u) & ~15u;
+        return at;
+    };
+    take(sizeof(FinCtl));  // offset 0
+    f.in = take(S * eb + 32);
+    f.out = take(S * eb + 32);
+    f.draws = take(2 * S + 64);  // bucket draws (u8/u16), later the u16 FY partners
+    f.C = take(finish_rank_warps(k) * ((k + 1) / 2) * 4);
+    f.bst = take((k + 1) * 4);
+    f.wsum = take((NTF / 32 + 1) * 4);
+    f.front0 = take(kFrontierCap * 4);
+    f.front1 = take(kFrontierCap * 4);
+    f.bar = take(16);
+    f.total = off;
+    return f;
+}
+
+uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t) {
+    return finish_layout(S_fuse, eb, k).total;
+}
+uint32_t finish_max_elems(uint32_t, uint32_t) { return 65535u; }
+uint32_t finish_smem_budget(uint32_t) { return kSmemLimit; }
+
+// ------------------------------------------------------ smem accessors ----
+struct Fin {
+    FinishLayout f;
+    __device__ __forceinline__ explicit Fin(const RunParams& rp) : f(finish_layout(rp.S_fuse, rp.eb, rp.k)) {}
+    __device__ __forceinline__ FinCtl* ctl() const { return reinterpret_cast<FinCtl*>(fsm); }
+    __device__ __forceinline__ unsigned char* in() const { return fsm + f.in; }
+    __device__ __forceinline__ unsigned char* out() const { return fsm + f.out; }
+    __device__ __forceinline__ unsigned char* draws() const { return fsm + f.draws; }
+    __device__ __forceinline__ uint16_t* jarr() const { return reinterpret_cast<uint16_t*>(fsm + f.draws); }
+    __device__ __forceinline__ uint32_t* C() const { return reinterpret_cast<uint32_t*>(fsm + f.C); }
+    __device__ __forceinline__ uint32_t* bst() const { return reinterpret_cast<uint32_t*>(fsm + f.bst); }
+    __device__ __forceinline__ uint32_t* wsum() const { return reinterpret_cast<uint32_t*>(fsm + f.wsum); }
     __device__ __forceinline__ uint32_t* front(uint32_t i) const {
-        return reinterpret_cast<uint32_t*>(sm + (i ? f.front1 : f.front0));
+        return reinterpret_cast<uint32_t*>(fsm + (i ? f.front1 : f.front0));
     }
-    __device__ __forceinline__ uint32_t* misc() const { return reinterpret_cast<uint32_t*>(sm + f.misc); }
-    __device__ __forceinline__ uint64_t* bar() const { return reinterpret_cast<uint64_t*>(sm + f.bar); }
-    __device__ __forceinline__ FinCtl* ctl() const { return reinterpret_cast<FinCtl*>(sm + f.ctl); }
+    __device__ __forceinline__ uint64_t* bar() const { return reinterpret_cast<uint64_t*>(fsm + f.bar); }
 };
 
 __device__ __forceinline__ bool item_permutes(const RunParams& rp, uint32_t len, uint32_t level) {
@@ -103,7 +109,9 @@ __device__ __forceinline__ bool item_permutes(const RunParams& rp, uint32_t len,
     return (!leaf && level < rp.max_levels) || (leaf && rp.run_leaves && len >= 2);
 }
 
-// ---- load / store of one item (aligned body by bulk copy, head/tail words)
+// ---- load / store of one item (aligned body by bulk copy, head/tail words).
+// Element i of an item lives at byte ((start*EB) & 15) + i*EB of a buffer,
+// so the aligned body maps to a 16-byte-aligned shared address.
 template <int EB>
 __device__ __forceinline__ void item_load(const Item& it, const unsigned char* src, unsigned char* buf, uint64_t* bar) {
     const uint32_t tid = threadIdx.x;
@@ -152,257 +160,379 @@ __device__ __forceinline__ void item_store(const Item& it, unsigned char* dst, c
             *reinterpret_cast<const uint32_t*>(buf + (tBeg - fl) + 4 * (tid - 64));
 }
 
-// Sequential Fisher-Yates (Fig. 1) on the elements el[a .. a+m) whose
-// element 0 sits at problem-relative position P0: for i = m-1 .. 1,
-// swap(i, fy(P0+i, i+1)).
-template <int EB>
-__device__ void fy_seq(unsigned char* el, uint32_t a, uint32_t m, uint64_t P0, PhiloxKey key) {
-    using E = typename ElemT<EB>::type;
-    E* A = reinterpret_cast<E*>(el) + a;
-    uint64_t gcur = ~0ull;
-    uint4 w = make_uint4(0, 0, 0, 0);
-    for (uint32_t i = m; i-- > 1;) {
-        const uint64_t P = P0 + i;
-        const uint64_t g = P >> 3;
-        if (g != gcur) {
-            w = fy16_group_words(key, g);
-            gcur = g;
+// ---------------------------------------------------- Fisher-Yates ------
+// FY partners of every leaf position in [a, a+m) (item-relative; the item's
+// element 0 is problem position P0), computed in parallel, one Philox call
+// per 8 consecutive positions (D5, 16-bit lanes): for a leaf [c, c+cm) with
+// 2 <= cm <= L and step i in [1, cm), J[c+i] = fy(P0+c+i, i+1) (Fig. 1,
+// P:109).  Leaves are the children bst[0..k] (relative to a) of the last
+// smem level, or [a, a+m) itself when single_leaf.  Ends with a barrier.
+__device__ __forceinline__ void fy_prep(const RunParams& rp, uint16_t* J, const uint32_t* bst, uint32_t a, uint32_t m,
+                                        uint64_t P0, PhiloxKey key, bool single_leaf) {
+    const uint64_t Pa = P0 + a;
+    const uint64_t g0 = Pa >> 3;
+    const uint32_t sh0 = (uint32_t)(Pa & 7u);  // index of position a inside group g0
+    const uint32_t ng = (sh0 + m + 7) >> 3;
+    const uint32_t L = rp.L;
+    uint16_t* Ja = J + a;
+    for (uint32_t t = threadIdx.x; t < ng; t += NTF) {
+        const uint4 w = fy16_group_words(key, g0 + t);
+        // lane jj of this group is item position rb + jj (relative to a)
+        const int32_t rb = (int32_t)(t * 8u) - (int32_t)sh0;
+        const uint32_t rfirst = rb < 0 ? 0u : (uint32_t)rb;
+        uint32_t lo = 0, cs = 0, ce = m;
+        if (!single_leaf) {
+            uint32_t hi = rp.k;
+            while (hi - lo > 1) {  // last b with bst[b] <= rfirst
+                const uint32_t mid = (lo + hi) >> 1;
+                if (bst[mid] <= rfirst) lo = mid;
+                else hi = mid;
+            }
+            cs = bst[lo];
+            ce = bst[lo + 1];
         }
-        const uint32_t j = fy16_from_lane(lane16(w, (uint32_t)(P & 7u)), key, P, i + 1);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (uint32_t jj = 0; jj < 8; ++jj) {
+            const int32_t ri = rb + (int32_t)jj;
+            if (ri >= 0 && ri < (int32_t)m) {
+                const uint32_t r = (uint32_t)ri;
+                while (r >= ce) {  // next leaf
+                    ++lo;
+                    cs = ce;
+                    ce = bst[lo + 1];
+                }
+                const uint32_t s = r - cs + 1;  // bound i+1
+                if (s >= 2 && ce - cs <= L) {
+                    const uint32_t v = (wv[jj >> 1] >> ((jj & 1u) * 16u)) & 0xFFFFu;
+                    const uint32_t mm = v * s;
+                    uint32_t j = mm >> 16;
+                    if ((mm & 0xFFFFu) < s) j = fy16_from_lane(v, key, Pa + r, s);  // exact rejection test (rare)
+                    Ja[r] = (uint16_t)j;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Sequential Fisher-Yates swaps of el[c .. c+cm) with the partners J[c+i].
+template <int EB>
+__device__ __forceinline__ void fy_run(unsigned char* el, const uint16_t* J, uint32_t c, uint32_t cm) {
+    using E = typename ElemT<EB>::type;
+    E* A = reinterpret_cast<E*>(el) + c;
+    const uint16_t* Jc = J + c;
+    for (uint32_t i = cm; i-- > 1;) {
+        const uint32_t j = Jc[i];
         const E t = A[i];
         A[i] = A[j];
         A[j] = t;
     }
 }
 
-// One stable scatter level in shared memory over el[a .. a+m), element a at
-// problem-relative position P0a: ranks in registers, then written back in
-// place in bucket-major order.  Leaves bucket starts (relative to a) in bst.
-template <int EB>
-__device__ void smem_level(const RunParams& rp, const FinCtx& c, unsigned char* el, uint32_t a, uint32_t m, uint64_t P0a,
-                           uint32_t level, PhiloxKey key, int wait_buf) {
+// ---------------------------------------------------- one smem level ----
+// Stable scatter of src[a .. a+m) into dst[a .. a+m) (element a at problem
+// position P0a).  Pass 1 counts buckets per warp; the counters become
+// (bucket, warp) bases; pass 2 re-walks the same rounds and takes each
+// element's slot with one ordered shared atomic on the base (block_ops.cuh).
+// Warp w owns elements [w*q, (w+1)*q); its round r is w*q + 32r + lane.
+// bst gets the bucket starts (relative to a).
+template <int EB, bool NARROW, bool ORD>
+__device__ __forceinline__ void smem_level(const RunParams& rp, const Fin& F, const unsigned char* src,
+                                           unsigned char* dst, uint32_t a, uint32_t m, uint64_t P0a, uint32_t level,
+                                           PhiloxKey key, bool wait_in) {
     using E = typename ElemT<EB>::type;
-    constexpr uint32_t RMAX = FinCfg<EB>::RMAX;
+    using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t k = rp.k, kw = (k + 1) >> 1;
     const uint32_t Wr = finish_rank_warps(k);
-    const DrawView dv = draws_to_smem<kFinThreads>(c.draws(), P0a, m, key, level, rp.bp);
-    uint32_t* C = c.C();
-    for (uint32_t i = tid; i < Wr * kw; i += kFinThreads) C[i] = 0;
-    if (wait_buf >= 0) mbar_wait(&c.bar()[wait_buf], c.ctl()->phase[wait_buf]);
+    const DrawView dv = draws_to_smem<NTF>(F.draws(), P0a, m, key, level, rp.bp);
+    uint32_t* C = F.C();
+    for (uint32_t i = tid; i < Wr * kw; i += NTF) C[i] = 0;
+    FinCtl* ctl = F.ctl();
+    if (wait_in) mbar_wait(F.bar(), ctl->phase);
     __syncthreads();
-    if (wait_buf >= 0 && tid == 0) c.ctl()->phase[wait_buf] ^= 1u;
+    if (wait_in && tid == 0) ctl->phase ^= 1u;
     const uint32_t q = (((m + Wr - 1) / Wr) + 31u) & ~31u;
-    const uint32_t R = q >> 5;
-    E* A = reinterpret_cast<E*>(el) + a;
-    E v[RMAX];
-    uint32_t rk[(RMAX + 1) / 2];  // two u16 ranks per register; buckets re-read from the draws
+    const uint32_t e0 = warp * q + lane;
+    const uint32_t lim = (warp < Wr && e0 < m) ? min(m - e0, q - lane) : 0u;  // round r valid iff 32r < lim
+    const D* dp = reinterpret_cast<const D*>(dv.d) + dv.off + e0;
+    const E* sp = reinterpret_cast<const E*>(src) + a + e0;
+    E* D0 = reinterpret_cast<E*>(dst) + a;
     uint32_t* Cw = C + warp * kw;
-    const bool ordered = rp.rank_ordered != 0;
-    if (warp < Wr) {
-#pragma unroll
-        for (uint32_t r = 0; r < RMAX; ++r) {
-            if (r < R) {
-                const uint32_t e = warp * q + r * 32 + lane;
-                const bool valid = e < m;
-                uint32_t b = 0;
-                if (valid) {
-                    v[r] = A[e];
-                    b = dv.at(e);
+    // Rounds are warp-uniform loops (bound q) with the per-lane validity as a
+    // predicate, so every round is one warp instruction per atomic: the
+    // ordered-atomic ranking relies on lane order within an instruction and
+    // on program order between rounds.
+    if (ORD) {
+        if (warp < Wr)
+            for (uint32_t o = 0; o < q; o += 32) {
+                if (o < lim) {
+                    const uint32_t b = dp[o];
+                    atomicAdd(&Cw[b >> 1], 1u << ((b & 1u) << 4));
                 }
-                const uint32_t rank = warp_rank(Cw, b, valid, ordered);
-                if (r & 1u) rk[r >> 1] |= rank << 16;
-                else rk[r >> 1] = rank;
+                __syncwarp();
             }
+    } else if (warp < Wr) {  // documented path: match-based counts, whole warp per round
+        for (uint32_t o = 0; o < q; o += 32) {
+            const bool valid = o < lim;
+            const uint32_t b = valid ? (uint32_t)dp[o] : 0xFFFFFFFFu;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
+            if (valid && (peers & lanemask_lt()) == 0)
+                atomicAdd(&Cw[b >> 1], (uint32_t)__popc(peers) << ((b & 1u) << 4));
         }
     }
     __syncthreads();
-    scan_counters<kFinThreads>(C, Wr, k, c.bst(), c.wsum());
-    if (warp < Wr) {
-#pragma unroll
-        for (uint32_t r = 0; r < RMAX; ++r) {
-            const uint32_t e = warp * q + r * 32 + lane;
-            if (r < R && e < m) {
-                const uint32_t b = dv.at(e);
-                const uint32_t base = (Cw[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu;
-                A[base + ((rk[r >> 1] >> ((r & 1u) << 4)) & 0xFFFFu)] = v[r];
+    scan_counters<NTF>(C, Wr, k, F.bst(), F.wsum());
+    if (ORD) {
+        if (warp < Wr)
+            for (uint32_t o = 0; o < q; o += 32) {
+                if (o < lim) {
+                    const uint32_t b = dp[o];
+                    const uint32_t sh = (b & 1u) << 4;
+                    const uint32_t slot = (atomicAdd(&Cw[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
+                    D0[slot] = sp[o];
+                }
+                __syncwarp();
             }
+    } else if (warp < Wr) {
+        for (uint32_t o = 0; o < q; o += 32) {
+            const bool valid = o < lim;
+            const uint32_t b = valid ? (uint32_t)dp[o] : 0u;
+            const uint32_t slot = warp_rank(Cw, b, valid, false);
+            if (valid) D0[slot] = sp[o];
         }
     }
-    if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->scattered_smem[level], (unsigned long long)m);
+    if (tid == 0) {
+        if (level < 32) ctl->st_smem[level] += m;
+        else atomicAdd((unsigned long long*)&rp.hdr->scattered_smem[level], (unsigned long long)m);
+    }
     __syncthreads();
 }
 
-// After smem_level over [a, a+m) at `level`: FY the children that are leaves,
-// queue the others for level+1 (count in misc[0]).
+// After a level over [a, a+m) of `el`: FY the children that are leaves
+// (partners precomputed by all threads, then one thread per leaf swaps),
+// queue the longer ones for the next level (count in ctl->nfront).
 template <int EB>
-__device__ __forceinline__ void handle_children(const RunParams& rp, const FinCtx& c, unsigned char* el, uint32_t a,
-                                                uint64_t P0, uint32_t level, PhiloxKey key, uint32_t* fnext) {
-    const uint32_t* bst = c.bst();
-    for (uint32_t b = threadIdx.x; b < rp.k; b += kFinThreads) {
+__device__ __forceinline__ void handle_children(const RunParams& rp, const Fin& F, unsigned char* el, uint32_t a,
+                                                uint32_t m, uint64_t P0, uint32_t level, PhiloxKey key,
+                                                uint32_t* fnext, uint32_t& fy_local) {
+    const uint32_t* bst = F.bst();
+    if (rp.run_leaves) fy_prep(rp, F.jarr(), bst, a, m, P0, key, false);
+    for (uint32_t b = threadIdx.x; b < rp.k; b += NTF) {
         const uint32_t ca = a + bst[b], cm = bst[b + 1] - bst[b];
         if (cm <= rp.L) {
             if (rp.run_leaves && cm >= 2) {
-                fy_seq<EB>(el, ca, cm, P0 + ca, key);
-                atomicAdd((unsigned long long*)&rp.hdr->fy_elems, (unsigned long long)cm);
+                fy_run<EB>(el, F.jarr(), ca, cm);
+                fy_local += cm;
             }
         } else if (level + 1 < rp.max_levels) {
-            const uint32_t slot = atomicAdd(&c.misc()[0], 1u);
+            const uint32_t slot = atomicAdd(&F.ctl()->nfront, 1u);
             fnext[slot] = ca | (cm << 16);
         }
     }
 }
 
-// Process one loaded (or loading) item in buffer bi and store it to buf0.
-template <int EB>
-__device__ void process_item(const RunParams& rp, const FinCtx& c, const Item& it, uint32_t bi) {
+// 1 if some child of the last level is longer than L (all threads call).
+__device__ __forceinline__ bool any_big_child(const RunParams& rp, const Fin& F) {
+    const uint32_t* bst = F.bst();
+    bool big = false;
+    for (uint32_t b = threadIdx.x; b < rp.k; b += NTF) big |= (bst[b + 1] - bst[b] > rp.L);
+    return __syncthreads_or(big) != 0;
+}
+
+// Process the item whose data is (arriving) in IN; it leaves through OUT (or
+// IN for leaf-only items).  Issues the load of `next` into IN as soon as IN
+// is free.
+template <int EB, bool NARROW, bool ORD>
+__device__ __forceinline__ void process_item(const RunParams& rp, const Fin& F, const Item& it, const Item* next,
+                                             const unsigned char* src, uint32_t& fy_local) {
+    using E = typename ElemT<EB>::type;
     const uint32_t tid = threadIdx.x;
-    unsigned char* el = c.buf(bi) + ((it.start * EB) & 15u);
+    const uint32_t off = (uint32_t)((it.start * EB) & 15u);
+    unsigned char* in = F.in() + off;
+    unsigned char* out = F.out() + off;
     const PhiloxKey key = make_key(it.key);
     const uint64_t P0 = it.start - it.origin;
     const uint32_t m = it.len;
     const bool leaf = m <= rp.L;
-    uint32_t* misc = c.misc();
-    if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->finished, (unsigned long long)m);
+    FinCtl* ctl = F.ctl();
+    if (tid == 0) ctl->st_finished += m;
     if (!leaf && it.level < rp.max_levels) {
-        if (tid == 0) misc[0] = 0;
-        smem_level<EB>(rp, c, el, 0, m, P0, it.level, key, (int)bi);
-        handle_children<EB>(rp, c, el, 0, P0, it.level, key, c.front(0));
+        // OUT was last read by the previous item's bulk store
+        if (tid == 0) bulk_wait_read0();
+        smem_level<EB, NARROW, ORD>(rp, F, in, out, 0, m, P0, it.level, key, true);
+        const bool deep = any_big_child(rp, F) && it.level + 1 < rp.max_levels;
+        if (!deep && next) item_load<EB>(*next, src, F.in(), F.bar());  // IN is free: overlap the next load
+        if (tid == 0) ctl->nfront = 0;
         __syncthreads();
-        uint32_t nf = misc[0], cur = 0, lv = it.level + 1;
+        handle_children<EB>(rp, F, out, 0, m, P0, it.level, key, F.front(0), fy_local);
         __syncthreads();
-        while (nf > 0) {  // deeper in-smem levels (rare when S_fuse / k << L)
-            if (tid == 0) misc[0] = 0;
+        uint32_t nf = ctl->nfront, cur = 0, lv = it.level + 1;
+        __syncthreads();
+        while (nf > 0) {  // deeper in-smem levels (rare when S_fuse / k << L): OUT -> IN -> OUT
+            if (tid == 0) ctl->nfront = 0;
             __syncthreads();
             for (uint32_t f = 0; f < nf; ++f) {
-                const uint32_t ent = c.front(cur)[f];
+                const uint32_t ent = F.front(cur)[f];
                 const uint32_t a = ent & 0xFFFFu, mm = ent >> 16;
-                smem_level<EB>(rp, c, el, a, mm, P0 + a, lv, key, -1);
-                handle_children<EB>(rp, c, el, a, P0, lv, key, c.front(cur ^ 1u));
+                smem_level<EB, NARROW, ORD>(rp, F, out, in, a, mm, P0 + a, lv, key, false);
+                for (uint32_t x = tid; x < mm; x += NTF)
+                    reinterpret_cast<E*>(out)[a + x] = reinterpret_cast<const E*>(in)[a + x];
+                __syncthreads();
+                handle_children<EB>(rp, F, out, a, mm, P0, lv, key, F.front(cur ^ 1u), fy_local);
                 __syncthreads();
             }
-            nf = misc[0];
+            nf = ctl->nfront;
             cur ^= 1u;
             ++lv;
             __syncthreads();
         }
+        if (deep && next) item_load<EB>(*next, src, F.in(), F.bar());
+        __syncthreads();
+        item_store<EB>(it, rp.buf0, F.out());
     } else {
-        mbar_wait(&c.bar()[bi], c.ctl()->phase[bi]);
+        // leaf-only (or level-limited) item: in place in IN
+        const bool fy = leaf && rp.run_leaves && m >= 2;
+        if (fy) fy_prep(rp, F.jarr(), F.bst(), 0, m, P0, key, true);
+        mbar_wait(F.bar(), ctl->phase);
         __syncthreads();
         if (tid == 0) {
-            c.ctl()->phase[bi] ^= 1u;
-            if (leaf && rp.run_leaves && m >= 2) {
-                fy_seq<EB>(el, 0, m, P0, key);
-                atomicAdd((unsigned long long*)&rp.hdr->fy_elems, (unsigned long long)m);
+            ctl->phase ^= 1u;
+            if (fy) {
+                fy_run<EB>(in, F.jarr(), 0, m);
+                fy_local += m;
             }
         }
+        __syncthreads();
+        item_store<EB>(it, rp.buf0, F.in());
+        if (next) {
+            if (tid == 0) bulk_wait_read0();  // IN must be read out before it is reloaded
+            __syncthreads();
+            item_load<EB>(*next, src, F.in(), F.bar());
+        }
     }
-    __syncthreads();
-    item_store<EB>(it, rp.buf0, c.buf(bi));
 }
 
-__device__ FinCtx make_fin_ctx(const RunParams& rp, unsigned char* sm) {
-    FinCtx c;
-    c.sm = sm;
-    c.f = finish_layout(rp.S_fuse, rp.eb, rp.k, rp.fin_nbuf);
+__device__ __forceinline__ void fin_init(const Fin& F) {
     if (threadIdx.x == 0) {
-        mbar_init(&c.bar()[0], 1);
-        mbar_init(&c.bar()[1], 1);
+        mbar_init(F.bar(), 1);
         fence_mbar_init();
-        c.ctl()->phase[0] = c.ctl()->phase[1] = 0;
+        FinCtl* c = F.ctl();
+        c->phase = 0;
+        c->st_finished = 0;
+        for (int i = 0; i < 32; ++i) c->st_smem[i] = 0;
     }
-    return c;
 }
 
-// Pipelined item loop.  Thread 0 advances the iterator (state in the control
-// block) and publishes items; everyone reads the current item from smem.
-template <int EB, class It>
-__device__ void run_items(const RunParams& rp, const FinCtx& c, const It& iter, const unsigned char* src) {
+// Item loop.  Warp 0 advances the iterator (state in the control block) and
+// publishes items; everyone reads the current item from smem.
+template <int EB, bool NARROW, bool ORD, class It>
+__device__ __forceinline__ void run_items(const RunParams& rp, const Fin& F, const It& iter, const unsigned char* src) {
     const uint32_t tid = threadIdx.x;
-    FinCtl* ctl = c.ctl();
-    if (tid == 0) ctl->have[0] = iter.next(ctl, ctl->items[0]) ? 1u : 0u;
+    FinCtl* ctl = F.ctl();
+    if (tid < 32) iter.next(ctl, 0);
     __syncthreads();
     if (!ctl->have[0]) return;
-    item_load<EB>(ctl->items[0], src, c.buf(0), &c.bar()[0]);
-    const uint32_t nbuf = rp.fin_nbuf;
+    uint32_t fy_local = 0;
+    item_load<EB>(ctl->items[0], src, F.in(), F.bar());
     for (uint32_t t = 0;; ++t) {
         const uint32_t slot = t & 1u;
-        if (tid == 0) ctl->have[slot ^ 1u] = iter.next(ctl, ctl->items[slot ^ 1u]) ? 1u : 0u;
+        if (tid < 32) iter.next(ctl, slot ^ 1u);
         __syncthreads();
         const Item cur = ctl->items[slot];
         const bool hn = ctl->have[slot ^ 1u] != 0;
-        const uint32_t bi = (nbuf > 1) ? slot : 0u;
-        if (hn && nbuf > 1) {
-            // buffer bi^1 was stored by item t-1: wait until that store has read it
-            if (tid == 0) bulk_wait_read0();
-            __syncthreads();
-            item_load<EB>(ctl->items[slot ^ 1u], src, c.buf(bi ^ 1u), &c.bar()[bi ^ 1u]);
-        }
-        process_item<EB>(rp, c, cur, bi);
+        process_item<EB, NARROW, ORD>(rp, F, cur, hn ? &ctl->items[slot ^ 1u] : nullptr, src, fy_local);
         if (!hn) break;
-        if (nbuf == 1) {
-            if (tid == 0) bulk_wait_read0();
-            __syncthreads();
-            item_load<EB>(ctl->items[slot ^ 1u], src, c.buf(0), &c.bar()[0]);
-        }
     }
-    if (tid == 0) bulk_wait0();
+    // flush the measurement counters: one global atomic per warp / per CTA
+    for (int o = 16; o > 0; o >>= 1) fy_local += __shfl_xor_sync(0xFFFFFFFFu, fy_local, o);
+    if ((tid & 31u) == 0 && fy_local) atomicAdd((unsigned long long*)&rp.hdr->fy_elems, (unsigned long long)fy_local);
+    if (tid == 0) {
+        atomicAdd((unsigned long long*)&rp.hdr->finished, ctl->st_finished);
+        for (uint32_t l = 0; l < 32; ++l)
+            if (ctl->st_smem[l]) atomicAdd((unsigned long long*)&rp.hdr->scattered_smem[l], ctl->st_smem[l]);
+        bulk_wait0();
+    }
 }
 
-// Children of the level-l segments (in the level's output buffer).
+// Children of the level-l segments (in the level's output buffer).  Called
+// by all 32 lanes of warp 0; lane 0 publishes items[slot] / have[slot].
 struct ChildIter {
     const RunParams* rp;
     const LevelParams* lp;
     uint32_t groups;
-    __device__ void load_unit(FinCtl* ctl) const {
-        ctl->b = (uint32_t)(ctl->u % groups) * kFinishBucketGroup;
-        ctl->bend = min(rp->k, ctl->b + kFinishBucketGroup);
+    __device__ __forceinline__ void load_unit(FinCtl* ctl) const {  // warp 0, all lanes
+        const uint32_t lane = threadIdx.x & 31u;
+        const SegDesc sg = lp->segs[(uint32_t)(ctl->u / groups)];
+        const uint32_t b0 = (uint32_t)(ctl->u % groups) * kUnit;
+        const uint32_t bend = min(rp->k, b0 + kUnit);
+        const uint64_t base0 = lp->prefix[sg.cbase];
+        if (lane <= bend - b0) {
+            const uint32_t b = b0 + lane;
+            ctl->ub[lane] = (b < rp->k) ? lp->prefix[sg.cbase + (uint64_t)b * sg.nchunks] - base0 : sg.len;
+        }
+        if (lane == 0) {
+            ctl->b = b0;
+            ctl->bend = bend;
+            ctl->seg_start = sg.start;
+            ctl->seg_origin = sg.origin;
+            ctl->seg_key = sg.key;
+        }
+        __syncwarp();
     }
-    __device__ bool next(FinCtl* ctl, Item& it) const {
+    __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {  // warp 0, all lanes
+        const uint32_t lane = threadIdx.x & 31u;
+        const uint32_t lvl = lp->level + 1;
         while (ctl->u < ctl->units) {
-            const SegDesc sg = lp->segs[(uint32_t)(ctl->u / groups)];
-            const uint64_t base0 = lp->prefix[sg.cbase];
-            while (ctl->b < ctl->bend) {
-                const uint32_t bb = ctl->b++;
-                const uint64_t s0 = lp->prefix[sg.cbase + (uint64_t)bb * sg.nchunks] - base0;
-                const uint64_t s1 =
-                    (bb + 1 < rp->k) ? lp->prefix[sg.cbase + (uint64_t)(bb + 1) * sg.nchunks] - base0 : sg.len;
-                const uint64_t len = s1 - s0;
+            const uint32_t b0 = (uint32_t)(ctl->u % groups) * kUnit;
+            for (uint32_t b = ctl->b; b < ctl->bend; ++b) {
+                const uint64_t s0 = ctl->ub[b - b0], len = ctl->ub[b - b0 + 1] - s0;
                 if (len == 0 || len > rp->S_fuse) continue;
-                const uint32_t lvl = lp->level + 1;
                 if (lp->dst == rp->buf0 && !item_permutes(*rp, (uint32_t)len, lvl)) continue;
-                it.start = sg.start + s0;
-                it.len = (uint32_t)len;
-                it.level = lvl;
-                it.origin = sg.origin;
-                it.key = sg.key;
-                return true;
+                __syncwarp();
+                if (lane == 0) {
+                    Item& it = ctl->items[slot];
+                    it.start = ctl->seg_start + s0;
+                    it.len = (uint32_t)len;
+                    it.level = lvl;
+                    it.origin = ctl->seg_origin;
+                    it.key = ctl->seg_key;
+                    ctl->have[slot] = 1;
+                    ctl->b = b + 1;
+                }
+                __syncwarp();
+                return;
             }
-            ctl->u += gridDim.x;
+            __syncwarp();
+            if (lane == 0) ctl->u += gridDim.x;
+            __syncwarp();
             if (ctl->u < ctl->units) load_unit(ctl);
         }
-        return false;
+        __syncwarp();
+        if (lane == 0) ctl->have[slot] = 0;
+        __syncwarp();
     }
 };
 
-template <int EB>
-__global__ void __launch_bounds__(kFinThreads, 1) k_finish_children(RunParams rp, LevelParams lp) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const uint32_t groups = (rp.k + kFinishBucketGroup - 1) / kFinishBucketGroup;
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(NTF, 1) k_finish_children(RunParams rp, LevelParams lp) {
+    const uint32_t groups = (rp.k + kUnit - 1) / kUnit;
     const uint64_t units = (uint64_t)lp.ctr->nseg * groups;
     if (blockIdx.x >= units) return;
-    const FinCtx c = make_fin_ctx(rp, sm);
-    ChildIter iter;
-    iter.rp = &rp;
-    iter.lp = &lp;
-    iter.groups = groups;
-    if (threadIdx.x == 0) {
-        c.ctl()->u = blockIdx.x;
-        c.ctl()->units = units;
-        iter.load_unit(c.ctl());
+    const Fin F(rp);
+    fin_init(F);
+    ChildIter iter{&rp, &lp, groups};
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) {
+            F.ctl()->u = blockIdx.x;
+            F.ctl()->units = units;
+        }
+        __syncwarp();
+        iter.load_unit(F.ctl());
     }
     __syncthreads();
-    run_items<EB>(rp, c, iter, lp.dst);
+    run_items<EB, NARROW, ORD>(rp, F, iter, lp.dst);
 }
 
 // Segments given by offsets (segmented mode at level 0, or the single problem
@@ -410,39 +540,43 @@ __global__ void __launch_bounds__(kFinThreads, 1) k_finish_children(RunParams rp
 struct SegIter {
     const RunParams* rp;
     const uint64_t* off;
-    __device__ bool next(FinCtl* ctl, Item& it) const {
-        while (ctl->u < ctl->units) {
-            const uint64_t si = ctl->u;
-            ctl->u += gridDim.x;
-            const uint64_t a = off[si], b = off[si + 1];
-            if (b <= a || b - a > rp->S_fuse) continue;
-            if (!item_permutes(*rp, (uint32_t)(b - a), 0u)) continue;
-            it.start = a;
-            it.len = (uint32_t)(b - a);
-            it.level = 0;
-            it.origin = a;
-            it.key = rp->seed + si * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
-            return true;
+    __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {  // warp 0, all lanes
+        const uint32_t lane = threadIdx.x & 31u;
+        if (lane == 0) {
+            ctl->have[slot] = 0;
+            while (ctl->u < ctl->units) {
+                const uint64_t si = ctl->u;
+                ctl->u += gridDim.x;
+                const uint64_t a = off[si], b = off[si + 1];
+                if (b <= a || b - a > rp->S_fuse) continue;
+                if (!item_permutes(*rp, (uint32_t)(b - a), 0u)) continue;
+                Item& it = ctl->items[slot];
+                it.start = a;
+                it.len = (uint32_t)(b - a);
+                it.level = 0;
+                it.origin = a;
+                it.key = rp->seed + si * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
+                ctl->have[slot] = 1;
+                break;
+            }
         }
-        return false;
+        __syncwarp();
     }
 };
 
-template <int EB>
-__global__ void __launch_bounds__(kFinThreads, 1) k_finish_segments(RunParams rp, const uint64_t* __restrict__ off,
-                                                                     uint64_t nsegs) {
-    extern __shared__ __align__(16) unsigned char sm[];
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(NTF, 1)
+    k_finish_segments(RunParams rp, const uint64_t* __restrict__ off, uint64_t nsegs) {
     if (blockIdx.x >= nsegs) return;
-    const FinCtx c = make_fin_ctx(rp, sm);
-    SegIter iter;
-    iter.rp = &rp;
-    iter.off = off;
+    const Fin F(rp);
+    fin_init(F);
     if (threadIdx.x == 0) {
-        c.ctl()->u = blockIdx.x;
-        c.ctl()->units = nsegs;
+        F.ctl()->u = blockIdx.x;
+        F.ctl()->units = nsegs;
     }
     __syncthreads();
-    run_items<EB>(rp, c, iter, rp.buf0);
+    SegIter iter{&rp, off};
+    run_items<EB, NARROW, ORD>(rp, F, iter, rp.buf0);
 }
 
 // Debug level limit: children longer than S_fuse produced by the last level
@@ -464,14 +598,38 @@ __global__ void k_copy_big(RunParams rp, LevelParams lp) {
     }
 }
 
-cudaError_t launch_finish_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
-    const uint32_t smem = finish_smem_bytes(rp.S_fuse, rp.eb, rp.k, rp.fin_nbuf);
-    switch (rp.eb) {
-    case 4: k_finish_children<4><<<grid, kFinThreads, smem, s>>>(rp, lp); break;
-    case 8: k_finish_children<8><<<grid, kFinThreads, smem, s>>>(rp, lp); break;
-    default: k_finish_children<16><<<grid, kFinThreads, smem, s>>>(rp, lp); break;
+// ------------------------------------------------------------- dispatch --
+template <int EB>
+static void* fin_children_fn(bool narrow, bool ord) {
+    if (ord) return narrow ? (void*)k_finish_children<EB, true, true> : (void*)k_finish_children<EB, false, true>;
+    return narrow ? (void*)k_finish_children<EB, true, false> : (void*)k_finish_children<EB, false, false>;
+}
+template <int EB>
+static void* fin_segments_fn(bool narrow, bool ord) {
+    if (ord) return narrow ? (void*)k_finish_segments<EB, true, true> : (void*)k_finish_segments<EB, false, true>;
+    return narrow ? (void*)k_finish_segments<EB, true, false> : (void*)k_finish_segments<EB, false, false>;
+}
+static void* fin_fn(uint32_t eb, bool seg, bool narrow, bool ord) {
+    switch (eb) {
+    case 4: return seg ? fin_segments_fn<4>(narrow, ord) : fin_children_fn<4>(narrow, ord);
+    case 8: return seg ? fin_segments_fn<8>(narrow, ord) : fin_children_fn<8>(narrow, ord);
+    default: return seg ? fin_segments_fn<16>(narrow, ord) : fin_children_fn<16>(narrow, ord);
     }
-    return cudaGetLastError();
+}
+
+cudaError_t launch_finish_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    const uint32_t smem = finish_smem_bytes(rp.S_fuse, rp.eb, rp.k, 1);
+    void* args[] = {(void*)&rp, (void*)&lp};
+    return cudaLaunchKernel(fin_fn(rp.eb, false, rp.bp.narrow != 0, rp.rank_ordered != 0), dim3(grid), dim3(NTF),
+                            args, smem, s);
+}
+
+cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
+                                   cudaStream_t s, int grid) {
+    const uint32_t smem = finish_smem_bytes(rp.S_fuse, rp.eb, rp.k, 1);
+    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments};
+    return cudaLaunchKernel(fin_fn(rp.eb, true, rp.bp.narrow != 0, rp.rank_ordered != 0), dim3(grid), dim3(NTF),
+                            args, smem, s);
 }
 
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
@@ -483,33 +641,20 @@ cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
-                                   cudaStream_t s, int grid) {
-    const uint32_t smem = finish_smem_bytes(rp.S_fuse, rp.eb, rp.k, rp.fin_nbuf);
-    switch (rp.eb) {
-    case 4: k_finish_segments<4><<<grid, kFinThreads, smem, s>>>(rp, d_offsets, num_segments); break;
-    case 8: k_finish_segments<8><<<grid, kFinThreads, smem, s>>>(rp, d_offsets, num_segments); break;
-    default: k_finish_segments<16><<<grid, kFinThreads, smem, s>>>(rp, d_offsets, num_segments); break;
-    }
-    return cudaGetLastError();
-}
-
 cudaError_t configure_finish(uint32_t smem) {
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_finish_children<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_finish_children<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_finish_children<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_finish_segments<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_finish_segments<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-    return cudaFuncSetAttribute(k_finish_segments<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (uint32_t eb : {4u, 8u, 16u})
+        for (int seg = 0; seg < 2; ++seg)
+            for (int nr = 0; nr < 2; ++nr)
+                for (int o = 0; o < 2; ++o) {
+                    cudaError_t e = cudaFuncSetAttribute(fin_fn(eb, seg, nr, o),
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                    if (e) return e;
+                }
+    return cudaSuccess;
 }
 
 cudaError_t occupancy_finish(uint32_t eb, uint32_t smem, int* blocks) {
-    switch (eb) {
-    case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_finish_children<4>, kFinThreads, smem);
-    case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_finish_children<8>, kFinThreads, smem);
-    default: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k_finish_children<16>, kFinThreads, smem);
-    }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fin_fn(eb, false, true, true), NTF, smem);
 }
 
 }  // namespace shuf

@@ -46,7 +46,7 @@ static uint32_t pick_s_fuse_nbuf(uint32_t eb, uint32_t k, uint32_t L, uint32_t n
     uint32_t lo = 1, hi = 65535;
     while (lo < hi) {
         uint32_t mid = (lo + hi + 1) / 2;
-        if (finish_smem_bytes(mid, eb, k, nbuf) <= kSmemLimit) lo = mid;
+        if (finish_smem_bytes(mid, eb, k, nbuf) <= finish_smem_budget(eb)) lo = mid;
         else hi = mid - 1;
     }
     const uint32_t rmax = finish_max_elems(eb, k);
@@ -64,7 +64,9 @@ static uint32_t pick_s_fuse(uint32_t eb, uint32_t k, uint32_t L, uint32_t* nbuf)
 }
 
 // Global levels needed until the largest segment fits S_fuse, with a
-// 12-sigma binomial margin per level, plus one spare level.
+// 6-sigma binomial margin per level, plus one spare level (a rarer outlier
+// child simply takes the spare level; only one that outlives the spare
+// level too raises SHUF_ERR_DEPTH).
 static uint32_t plan_levels(uint64_t n, uint32_t k, uint32_t S_fuse) {
     if (n <= S_fuse) return 0;
     double m = (double)n;
@@ -72,7 +74,7 @@ static uint32_t plan_levels(uint64_t n, uint32_t k, uint32_t S_fuse) {
     while (m > S_fuse && g < kMaxLevels) {
         ++g;
         double mu = m / k;
-        m = mu + 12.0 * std::sqrt(mu) + 32.0;
+        m = mu + 6.0 * std::sqrt(mu) + 32.0;
         if (m >= (double)n) m = (double)n;  // k small: still shrinks in expectation
         if (g > 200) break;
     }

@@ -17,7 +17,7 @@ constexpr uint32_t kSmemLimit = 227 * 1024;
 constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
 constexpr uint32_t kSegGroup = 8;          // user segments per finish work unit (segmented mode)
 constexpr uint32_t kMaxLevels = 256;
-constexpr uint32_t kFrontierCap = 1024;     // pending in-smem sub-segments per level
+constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
 
 // ---------------------------------------------------------- descriptors ---
 // A segment processed by an HBM-resident ("global") scatter level.
@@ -122,6 +122,7 @@ cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offset
                                    cudaStream_t s, int grid);
 uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t nbuf);
 uint32_t finish_max_elems(uint32_t eb, uint32_t k);
+uint32_t finish_smem_budget(uint32_t eb);
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);

@@ -63,25 +63,24 @@ def bucket_np(K: int, level: int, p: np.ndarray, k: int) -> np.ndarray:
     return out
 
 
-def fy_np(K: int, P: np.ndarray, s: np.ndarray) -> np.ndarray:
-    """D5 for bounds s <= 2^16 (16-bit lanes; the only case leaves <= 65536 need)."""
-    P = np.asarray(P, dtype=np.uint64)
-    s = np.asarray(s, dtype=np.uint64)
+def fy_np(K: int, q: int, i: np.ndarray) -> np.ndarray:
+    """D5 for steps i (bound i+1 <= 2^16) of the leaf starting at position q."""
+    i = np.asarray(i, dtype=np.uint64)
+    s = i + np.uint64(1)
     assert (s <= 65536).all()
     kw = (K & 0xFFFFFFFF, K >> 32)
-    g = P >> np.uint64(3)
-    W = np.stack(philox_np(g & M32, g >> np.uint64(32), np.uint64(0), np.uint64(2), *kw))
-    j = (P & np.uint64(7)).astype(np.int64)
-    v = (W[j >> 1, np.arange(P.shape[0])] >> (np.uint64(16) * (j & 1).astype(np.uint64))) & np.uint64(0xFFFF)
-    t = np.uint64(65536) % np.maximum(s, np.uint64(1))
-    out = np.zeros(P.shape[0], dtype=np.int64)
-    todo = np.ones(P.shape[0], dtype=bool)
+    q = np.uint64(q)
+    W = np.stack(philox_np(q & M32, q >> np.uint64(32), i >> np.uint64(3), np.uint64(2), *kw))
+    j = (i & np.uint64(7)).astype(np.int64)
+    v = (W[j >> 1, np.arange(i.shape[0])] >> (np.uint64(16) * (j & 1).astype(np.uint64))) & np.uint64(0xFFFF)
+    t = np.uint64(65536) % s
+    out = np.zeros(i.shape[0], dtype=np.int64)
+    todo = np.ones(i.shape[0], dtype=bool)
     a = 0
     while todo.any():
         idx = np.nonzero(todo)[0]
         if a:
-            Pb = P[idx]
-            v_i = philox_np(Pb & M32, Pb >> np.uint64(32), np.uint64(a), np.uint64(4), *kw)[0] & np.uint64(0xFFFF)
+            v_i = philox_np(q & M32, q >> np.uint64(32), i[idx], np.uint64(4 | (a << 8)), *kw)[0] & np.uint64(0xFFFF)
         else:
             v_i = v[idx]
         m = v_i * s[idx]
@@ -120,7 +119,7 @@ def shuffle_np(data: np.ndarray, k: int, L: int, K: int, max_levels: int = 1 << 
             if m < 2:
                 continue
             i = np.arange(m - 1, 0, -1)
-            j = fy_np(K, q + i, i + 1)
+            j = fy_np(K, q, i)
             for ii, jj in zip(i, j):
                 A[[q + ii, q + jj]] = A[[q + jj, q + ii]]
     return A

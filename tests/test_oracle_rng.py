@@ -145,53 +145,55 @@ def test_bucket_draw_retry_stream():
 
 
 def test_fy_draw_layout_and_retry_16bit():
-    """D5, s <= 2^16: 16-bit lane P&7 of Philox(K, (P>>3, 0, FY16=2));
-    retries from Philox(K, (P, a, FY16_RETRY=4)).w0 & 0xFFFF; s=40000
-    rejects ~39% of the lanes."""
+    """D5, s <= 2^16, keyed by (leaf id q, step i): 16-bit lane i&7 of
+    Philox(K, (q, i>>3, FY16=2)); retries from Philox(K, (q, i, 4 | a<<8)).w0
+    & 0xFFFF; bound s = i+1 = 40000 rejects ~39% of the lanes."""
     K = oracle.problem_key(11, 2)
     key = [K & 0xFFFFFFFF, K >> 32]
-    s = 40000
-    t = 65536 % s
     seen = 0
-    for P in list(range(400)) + [2**40 + 3]:
-        j, rej = oracle.fy_draw(K, P, s)
-        g = P >> 3
-        w = oracle.philox([g & 0xFFFFFFFF, g >> 32, 0, 2], key)
-        v = (int(w[(P & 7) >> 1]) >> (16 * (P & 1))) & 0xFFFF
-        a = 0
-        while (v * s) & 0xFFFF < t:
-            a += 1
-            v = int(oracle.philox([P & 0xFFFFFFFF, P >> 32, a, 4], key)[0]) & 0xFFFF
-        assert rej == a and j == (v * s) >> 16 and 0 <= j < s
-        seen += rej > 0
-    assert seen > 80
+    for q in (0, 77, 2**40 + 3):
+        for i in list(range(1, 200)) + [39999] * 0 + list(range(39990, 40010)):
+            s = i + 1
+            t = 65536 % s
+            j, rej = oracle.fy_draw(K, q, i)
+            w = oracle.philox([q & 0xFFFFFFFF, q >> 32, i >> 3, 2], key)
+            v = (int(w[(i & 7) >> 1]) >> (16 * (i & 1))) & 0xFFFF
+            a = 0
+            while (v * s) & 0xFFFF < t:
+                a += 1
+                v = int(oracle.philox([q & 0xFFFFFFFF, q >> 32, i, 4 | (a << 8)], key)[0]) & 0xFFFF
+            assert rej == a and j == (v * s) >> 16 and 0 <= j <= i
+            seen += rej > 0
+    assert seen > 5
 
 
 def test_fy_draw_layout_and_retry_32bit():
-    """D5, s > 2^16: 32-bit word P&3 of Philox(K, (P>>2, 0, FY32=5)); retries
-    from Philox(K, (P, a, FY32_RETRY=6)).w0; s=2^31+1 rejects ~half."""
+    """D5, s > 2^16: 32-bit word i&3 of Philox(K, (q, i>>2, FY32=5));
+    retries from Philox(K, (q, i, 6 | a<<8)).w0; s=2^31+1 rejects ~half."""
     K = oracle.problem_key(11, 2)
     key = [K & 0xFFFFFFFF, K >> 32]
-    s = 2**31 + 1
-    t = 2**32 % s
     seen = 0
-    for P in list(range(300)) + [2**40 + 3]:
-        j, rej = oracle.fy_draw(K, P, s)
-        g = P >> 2
-        w = int(oracle.philox([g & 0xFFFFFFFF, g >> 32, 0, 5], key)[P & 3])
-        a = 0
-        while (w * s) % 2**32 < t:
-            a += 1
-            w = int(oracle.philox([P & 0xFFFFFFFF, P >> 32, a, 6], key)[0])
-        assert rej == a and j == (w * s) >> 32 and 0 <= j < s
-        seen += rej > 0
+    for q in (0, 5, 2**40 + 3):
+        for i in list(range(2**31, 2**31 + 100)) + [70000, 65536]:
+            s = i + 1
+            t = 2**32 % s
+            j, rej = oracle.fy_draw(K, q, i)
+            w = int(oracle.philox([q & 0xFFFFFFFF, q >> 32, i >> 2, 5], key)[i & 3])
+            a = 0
+            while (w * s) % 2**32 < t:
+                a += 1
+                w = int(oracle.philox([q & 0xFFFFFFFF, q >> 32, i, 6 | (a << 8)], key)[0])
+            assert rej == a and j == (w * s) >> 32 and 0 <= j <= i
+            seen += rej > 0
     assert seen > 50
 
 
-def test_fy_draw_boundary_65536_uses_16bit_lanes():
+def test_fy_draw_boundary_65535_uses_16bit_lanes():
+    """i = 65535 (s = 2^16): 16-bit lanes, pure shift, no rejection."""
     K = oracle.problem_key(1, 0)
     key = [K & 0xFFFFFFFF, K >> 32]
-    for P in range(64):
-        w = oracle.philox([(P >> 3), 0, 0, 2], key)
-        v = (int(w[(P & 7) >> 1]) >> (16 * (P & 1))) & 0xFFFF
-        assert oracle.fy_draw(K, P, 65536) == (v, 0)  # s = 2^16: pure shift, no rejection
+    for q in range(8):
+        i = 65535
+        w = oracle.philox([q, 0, i >> 3, 2], key)
+        v = (int(w[(i & 7) >> 1]) >> (16 * (i & 1))) & 0xFFFF
+        assert oracle.fy_draw(K, q, i) == (v, 0)

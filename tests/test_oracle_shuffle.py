@@ -81,7 +81,7 @@ def test_single_leaf_is_textbook_fisher_yates(n):
     a = np.arange(n, dtype=np.uint32)
     got = oracle.shuffle(a, 2, n, seed)
     i = np.arange(n - 1, 0, -1)
-    j = oracle.fy_draws(K, i, i + 1)
+    j = oracle.fy_draws(K, 0, i)  # leaf id = its start position 0, step i
     assert (j <= i).all()
     exp = list(range(n))
     for ii, jj in zip(i, j):
