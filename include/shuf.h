@@ -94,9 +94,10 @@ shuf_status shuf_debug_run_levels(shuf_plan_t p, void *ptr, void *scratch, uint6
 shuf_status shuf_debug_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count, uint32_t k,
                                     uint32_t *d_out, void *stream);
 
-/* Test hook: out[i] = D5 Fisher-Yates draw at position d_P[i] with bound
- * d_s[i] (>= 1) under key K; device arrays of count elements. */
-shuf_status shuf_debug_fy_draws(uint64_t K, const uint64_t *d_P, const uint32_t *d_s, uint64_t count,
+/* Test hook: out[x] = D5 Fisher-Yates partner of step d_i[x] (bound
+ * d_i[x]+1) of the leaf starting at problem position d_q[x], under key K;
+ * device arrays of count elements. */
+shuf_status shuf_debug_fy_draws(uint64_t K, const uint64_t *d_q, const uint32_t *d_i, uint64_t count,
                                 uint32_t *d_out, void *stream);
 
 /* Kernel classes reported by shuf_profile_run. */

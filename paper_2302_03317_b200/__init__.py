@@ -193,8 +193,9 @@ def shuf_debug_bucket_draws(K: int, level: int, p0: int, count: int, k: int, out
            "shuf_debug_bucket_draws")
 
 
-def shuf_debug_fy_draws(K: int, P, s, out, stream=None):
-    _check(lib().shuf_debug_fy_draws(K % (1 << 64), _dev_ptr(P, "P"), _dev_ptr(s, "s"), P.numel(),
+def shuf_debug_fy_draws(K: int, q, i, out, stream=None):
+    """D5 partners of steps i of the leaves starting at q (device arrays)."""
+    _check(lib().shuf_debug_fy_draws(K % (1 << 64), _dev_ptr(q, "q"), _dev_ptr(i, "i"), q.numel(),
                                      _dev_ptr(out, "out"), _stream(stream)), "shuf_debug_fy_draws")
 
 

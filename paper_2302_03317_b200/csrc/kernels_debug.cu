@@ -14,10 +14,10 @@ __global__ void k_debug_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, ui
         out[i] = bucket_draw(key, level, p0 + i, bp);
 }
 
-__global__ void k_debug_fy_draws(uint64_t K, const uint64_t* P, const uint32_t* s, uint64_t count, uint32_t* out) {
+__global__ void k_debug_fy_draws(uint64_t K, const uint64_t* q, const uint32_t* step, uint64_t count, uint32_t* out) {
     const PhiloxKey key = make_key(K);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = fy_draw(key, P[i], s[i]);
+        out[i] = fy_draw(key, q[i], step[i]);
 }
 
 // Probe: do same-address shared atomicAdds of one warp instruction return in

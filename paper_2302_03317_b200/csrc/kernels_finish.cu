@@ -69,7 +69,7 @@ __host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, u
     take(sizeof(FinCtl));  // offset 0
     f.in = take(S * eb + 32);
     f.out = take(S * eb + 32);
-    f.draws = take(2 * S + 64);  // bucket draws (u8/u16), later the u16 FY partners
+    f.draws = take(2 * S + 64);  // bucket draws (u8 / u16)
     f.C = take(finish_rank_warps(k) * ((k + 1) / 2) * 4);
     f.bst = take((k + 1) * 4);
     f.wsum = take((NTF / 32 + 1) * 4);
@@ -94,7 +94,6 @@ struct Fin {
     __device__ __forceinline__ unsigned char* in() const { return fsm + f.in; }
     __device__ __forceinline__ unsigned char* out() const { return fsm + f.out; }
     __device__ __forceinline__ unsigned char* draws() const { return fsm + f.draws; }
-    __device__ __forceinline__ uint16_t* jarr() const { return reinterpret_cast<uint16_t*>(fsm + f.draws); }
     __device__ __forceinline__ uint32_t* C() const { return reinterpret_cast<uint32_t*>(fsm + f.C); }
     __device__ __forceinline__ uint32_t* bst() const { return reinterpret_cast<uint32_t*>(fsm + f.bst); }
     __device__ __forceinline__ uint32_t* wsum() const { return reinterpret_cast<uint32_t*>(fsm + f.wsum); }
@@ -161,72 +160,51 @@ __device__ __forceinline__ void item_store(const Item& it, unsigned char* dst, c
 }
 
 // ---------------------------------------------------- Fisher-Yates ------
-// FY partners of every leaf position in [a, a+m) (item-relative; the item's
-// element 0 is problem position P0), computed in parallel, one Philox call
-// per 8 consecutive positions (D5, 16-bit lanes): for a leaf [c, c+cm) with
-// 2 <= cm <= L and step i in [1, cm), J[c+i] = fy(P0+c+i, i+1) (Fig. 1,
-// P:109).  Leaves are the children bst[0..k] (relative to a) of the last
-// smem level, or [a, a+m) itself when single_leaf.  Ends with a barrier.
-__device__ __forceinline__ void fy_prep(const RunParams& rp, uint16_t* J, const uint32_t* bst, uint32_t a, uint32_t m,
-                                        uint64_t P0, PhiloxKey key, bool single_leaf) {
-    const uint64_t Pa = P0 + a;
-    const uint64_t g0 = Pa >> 3;
-    const uint32_t sh0 = (uint32_t)(Pa & 7u);  // index of position a inside group g0
-    const uint32_t ng = (sh0 + m + 7) >> 3;
-    const uint32_t L = rp.L;
-    uint16_t* Ja = J + a;
-    for (uint32_t t = threadIdx.x; t < ng; t += NTF) {
-        const uint4 w = fy16_group_words(key, g0 + t);
-        // lane jj of this group is item position rb + jj (relative to a)
-        const int32_t rb = (int32_t)(t * 8u) - (int32_t)sh0;
-        const uint32_t rfirst = rb < 0 ? 0u : (uint32_t)rb;
-        uint32_t lo = 0, cs = 0, ce = m;
-        if (!single_leaf) {
-            uint32_t hi = rp.k;
-            while (hi - lo > 1) {  // last b with bst[b] <= rfirst
-                const uint32_t mid = (lo + hi) >> 1;
-                if (bst[mid] <= rfirst) lo = mid;
-                else hi = mid;
-            }
-            cs = bst[lo];
-            ce = bst[lo + 1];
-        }
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (uint32_t jj = 0; jj < 8; ++jj) {
-            const int32_t ri = rb + (int32_t)jj;
-            if (ri >= 0 && ri < (int32_t)m) {
-                const uint32_t r = (uint32_t)ri;
-                while (r >= ce) {  // next leaf
-                    ++lo;
-                    cs = ce;
-                    ce = bst[lo + 1];
-                }
-                const uint32_t s = r - cs + 1;  // bound i+1
-                if (s >= 2 && ce - cs <= L) {
-                    const uint32_t v = (wv[jj >> 1] >> ((jj & 1u) * 16u)) & 0xFFFFu;
-                    const uint32_t mm = v * s;
-                    uint32_t j = mm >> 16;
-                    if ((mm & 0xFFFFu) < s) j = fy16_from_lane(v, key, Pa + r, s);  // exact rejection test (rare)
-                    Ja[r] = (uint16_t)j;
-                }
-            }
-        }
-    }
-    __syncthreads();
+// One Fisher-Yates step (Fig. 1): swap(A[i], A[j]), j = fy(q, i) from the
+// 16-bit lane v of the step's Philox group (D5, Lemire16).
+template <typename E>
+__device__ __forceinline__ void fy_step(E* A, uint32_t i, uint32_t v, PhiloxKey key, uint64_t q) {
+    const uint32_t s = i + 1, mm = v * s;
+    uint32_t j = mm >> 16;
+    if (__builtin_expect((mm & 0xFFFFu) < s, 0)) j = fy16_from_lane(v, key, q, i);  // exact rejection test
+    const E t = A[i];
+    A[i] = A[j];
+    A[j] = t;
 }
 
-// Sequential Fisher-Yates swaps of el[c .. c+cm) with the partners J[c+i].
+// Fisher-Yates (Fig. 1) of the leaf A[0 .. cm) whose first
+// element is problem position q: for i = cm-1 .. 1, swap(i, fy(q, i)) with
+// the partner drawn for (leaf id q, step i) (D5): one Philox call per 8
+// steps, so every lane of a warp (each on its own leaf) draws in lockstep.
+// The partial top group is peeled so the full groups run without checks.
 template <int EB>
-__device__ __forceinline__ void fy_run(unsigned char* el, const uint16_t* J, uint32_t c, uint32_t cm) {
+__device__ __forceinline__ void fy_leaf(unsigned char* el, uint32_t c, uint32_t cm, uint64_t q, PhiloxKey key) {
     using E = typename ElemT<EB>::type;
+    if (cm < 2) return;
     E* A = reinterpret_cast<E*>(el) + c;
-    const uint16_t* Jc = J + c;
-    for (uint32_t i = cm; i-- > 1;) {
-        const uint32_t j = Jc[i];
-        const E t = A[i];
-        A[i] = A[j];
-        A[j] = t;
+    const uint32_t gt = (cm - 1) >> 3;
+    {  // top group: steps cm-1 .. max(8*gt, 1)
+        const uint4 w = fy16_group_words(key, q, gt);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int32_t jj = 7; jj >= 0; --jj) {
+            const uint32_t i = gt * 8u + (uint32_t)jj;
+            if (i < cm && i >= 1) fy_step(A, i, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+        }
+    }
+    for (int32_t g = (int32_t)gt - 1; g >= 1; --g) {  // full groups
+        const uint4 w = fy16_group_words(key, q, (uint32_t)g);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+        E* Ag = A;
+#pragma unroll
+        for (int32_t jj = 7; jj >= 0; --jj)
+            fy_step(Ag, (uint32_t)g * 8u + (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+    }
+    if (gt >= 1) {  // group 0: steps 7 .. 1
+        const uint4 w = fy16_group_words(key, q, 0u);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int32_t jj = 7; jj >= 1; --jj) fy_step(A, (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
     }
 }
 
@@ -256,23 +234,25 @@ __device__ __forceinline__ void smem_level(const RunParams& rp, const Fin& F, co
     const uint32_t q = (((m + Wr - 1) / Wr) + 31u) & ~31u;
     const uint32_t e0 = warp * q + lane;
     const uint32_t lim = (warp < Wr && e0 < m) ? min(m - e0, q - lane) : 0u;  // round r valid iff 32r < lim
-    const D* dp = reinterpret_cast<const D*>(dv.d) + dv.off + e0;
+    // per-lane bases, computed once; draw offset of position a = P0a mod group
+    const uint32_t doff = (uint32_t)(P0a & (NARROW ? 15u : 7u));
+    const D* dp = reinterpret_cast<const D*>(fsm + F.f.draws) + doff + e0;
     const E* sp = reinterpret_cast<const E*>(src) + a + e0;
     E* D0 = reinterpret_cast<E*>(dst) + a;
     uint32_t* Cw = C + warp * kw;
     // Rounds are warp-uniform loops (bound q) with the per-lane validity as a
-    // predicate, so every round is one warp instruction per atomic: the
-    // ordered-atomic ranking relies on lane order within an instruction and
-    // on program order between rounds.
+    // predicate (an invalid lane adds 0), so every round is exactly one warp
+    // instruction per atomic: the ordered-atomic ranking relies on lane
+    // order within an instruction and on program order between rounds.
     if (ORD) {
-        if (warp < Wr)
+        if (warp < Wr) {
+#pragma unroll 4
             for (uint32_t o = 0; o < q; o += 32) {
-                if (o < lim) {
-                    const uint32_t b = dp[o];
-                    atomicAdd(&Cw[b >> 1], 1u << ((b & 1u) << 4));
-                }
-                __syncwarp();
+                const bool valid = o < lim;
+                const uint32_t b = dp[valid ? o : 0u];
+                atomicAdd(&Cw[b >> 1], valid ? (1u << ((b & 1u) << 4)) : 0u);
             }
+        }
     } else if (warp < Wr) {  // documented path: match-based counts, whole warp per round
         for (uint32_t o = 0; o < q; o += 32) {
             const bool valid = o < lim;
@@ -285,16 +265,18 @@ __device__ __forceinline__ void smem_level(const RunParams& rp, const Fin& F, co
     __syncthreads();
     scan_counters<NTF>(C, Wr, k, F.bst(), F.wsum());
     if (ORD) {
-        if (warp < Wr)
+        if (warp < Wr) {
+#pragma unroll 4
             for (uint32_t o = 0; o < q; o += 32) {
-                if (o < lim) {
-                    const uint32_t b = dp[o];
-                    const uint32_t sh = (b & 1u) << 4;
-                    const uint32_t slot = (atomicAdd(&Cw[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
-                    D0[slot] = sp[o];
-                }
-                __syncwarp();
+                const bool valid = o < lim;
+                const uint32_t oo = valid ? o : 0u;
+                const uint32_t b = dp[oo];
+                const uint32_t sh = (b & 1u) << 4;
+                const E x = sp[oo];
+                const uint32_t slot = (atomicAdd(&Cw[b >> 1], valid ? (1u << sh) : 0u) >> sh) & 0xFFFFu;
+                if (valid) D0[slot] = x;
             }
+        }
     } else if (warp < Wr) {
         for (uint32_t o = 0; o < q; o += 32) {
             const bool valid = o < lim;
@@ -310,20 +292,18 @@ __device__ __forceinline__ void smem_level(const RunParams& rp, const Fin& F, co
     __syncthreads();
 }
 
-// After a level over [a, a+m) of `el`: FY the children that are leaves
-// (partners precomputed by all threads, then one thread per leaf swaps),
-// queue the longer ones for the next level (count in ctl->nfront).
+// After a level over [a, a+m) of `el`: FY the children that are leaves (one
+// thread per leaf), queue the longer ones for the next level (ctl->nfront).
 template <int EB>
 __device__ __forceinline__ void handle_children(const RunParams& rp, const Fin& F, unsigned char* el, uint32_t a,
                                                 uint32_t m, uint64_t P0, uint32_t level, PhiloxKey key,
                                                 uint32_t* fnext, uint32_t& fy_local) {
     const uint32_t* bst = F.bst();
-    if (rp.run_leaves) fy_prep(rp, F.jarr(), bst, a, m, P0, key, false);
     for (uint32_t b = threadIdx.x; b < rp.k; b += NTF) {
         const uint32_t ca = a + bst[b], cm = bst[b + 1] - bst[b];
         if (cm <= rp.L) {
             if (rp.run_leaves && cm >= 2) {
-                fy_run<EB>(el, F.jarr(), ca, cm);
+                fy_leaf<EB>(el, ca, cm, P0 + ca, key);
                 fy_local += cm;
             }
         } else if (level + 1 < rp.max_levels) {
@@ -394,13 +374,12 @@ __device__ __forceinline__ void process_item(const RunParams& rp, const Fin& F, 
     } else {
         // leaf-only (or level-limited) item: in place in IN
         const bool fy = leaf && rp.run_leaves && m >= 2;
-        if (fy) fy_prep(rp, F.jarr(), F.bst(), 0, m, P0, key, true);
         mbar_wait(F.bar(), ctl->phase);
         __syncthreads();
         if (tid == 0) {
             ctl->phase ^= 1u;
             if (fy) {
-                fy_run<EB>(in, F.jarr(), 0, m);
+                fy_leaf<EB>(in, 0, m, P0, key);
                 fy_local += m;
             }
         }

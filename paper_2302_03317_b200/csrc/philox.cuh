@@ -12,11 +12,11 @@
 //      otherwise ("wide"): 16-bit lane p&7 of Philox(K, (p>>3, l, SC=1)),
 //        Lemire with threshold 2^16 mod k, retries from
 //        Philox(K, (p, l | a<<8, SC_RETRY=3)).w0 & 0xFFFF.
-//   D5 FY draw at (position P, bound s):
-//      s <= 2^16: 16-bit lane P&7 of Philox(K, (P>>3, 0, FY16=2)), Lemire16,
-//        retries from Philox(K, (P, a, FY16_RETRY=4)).w0 & 0xFFFF;
-//      s >  2^16: word P&3 of Philox(K, (P>>2, 0, FY32=5)), Lemire32,
-//        retries from Philox(K, (P, a, FY32_RETRY=6)).w0.
+//   D5 FY draw for step i (bound s = i+1) of the leaf starting at q:
+//      s <= 2^16: 16-bit lane i&7 of Philox(K, (q, i>>3, FY16=2)), Lemire16,
+//        retries from Philox(K, (q, i, FY16_RETRY=4 | a<<8)).w0 & 0xFFFF;
+//      s >  2^16: word i&3 of Philox(K, (q, i>>2, FY32=5)), Lemire32,
+//        retries from Philox(K, (q, i, FY32_RETRY=6 | a<<8)).w0.
 //   Fig. 1: partner = gen_index(rng, i+1), i.e. s = i + 1.
 #pragma once
 #include <cstdint>
@@ -120,45 +120,48 @@ __device__ __forceinline__ uint32_t bucket_draw(PhiloxKey key, uint32_t level, u
 }
 
 // ---------------------------------------------------------------- D5 ----
-__device__ __forceinline__ uint4 fy16_group_words(PhiloxKey key, uint64_t g) {
-    return philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, TAG_FY16), key);
+// Partner of step i (bound s = i+1) of the leaf starting at problem-relative
+// position q, keyed by (seed, leaf id q, step i).
+__device__ __forceinline__ uint4 fy16_group_words(PhiloxKey key, uint64_t q, uint32_t grp) {
+    return philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), grp, TAG_FY16), key);
 }
 
-static __device__ __noinline__ uint32_t fy16_retry(PhiloxKey key, uint64_t P, uint32_t s) {
-    const uint32_t t = 65536u % s;
+static __device__ __noinline__ uint32_t fy16_retry(PhiloxKey key, uint64_t q, uint32_t i) {
+    const uint32_t s = i + 1, t = 65536u % s;
     for (uint32_t a = 1;; ++a) {
-        uint4 w = philox4x32_10(make_uint4((uint32_t)P, (uint32_t)(P >> 32), a, TAG_FY16_RETRY), key);
+        uint4 w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), i, TAG_FY16_RETRY | (a << 8)), key);
         const uint32_t m = (w.x & 0xFFFFu) * s;
         if ((m & 0xFFFFu) >= t) return m >> 16;
     }
 }
 
-// Lemire16 on lane v of position P with bound s <= 2^16; the modulo is only
+// Lemire16 on lane v for step i (s = i+1 <= 2^16); the modulo is only
 // evaluated when the cheap pre-check (low part < s) cannot rule rejection out.
-__device__ __forceinline__ uint32_t fy16_from_lane(uint32_t v, PhiloxKey key, uint64_t P, uint32_t s) {
+__device__ __forceinline__ uint32_t fy16_from_lane(uint32_t v, PhiloxKey key, uint64_t q, uint32_t i) {
+    const uint32_t s = i + 1;
     const uint32_t m = v * s;
     const uint32_t lo = m & 0xFFFFu;
-    if (lo < s && lo < 65536u % s) return fy16_retry(key, P, s);
+    if (lo < s && lo < 65536u % s) return fy16_retry(key, q, i);
     return m >> 16;
 }
 
-static __device__ __noinline__ uint32_t fy32_draw(PhiloxKey key, uint64_t P, uint32_t s) {
+static __device__ __noinline__ uint32_t fy32_draw(PhiloxKey key, uint64_t q, uint32_t i) {
+    const uint32_t s = i + 1;
     const uint32_t t = (uint32_t)(0x100000000ull % s);
-    const uint64_t g = P >> 2;
-    uint4 w = philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, TAG_FY32), key);
-    uint64_t M = (uint64_t)word_of(w, (uint32_t)(P & 3u)) * s;
+    uint4 w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), i >> 2, TAG_FY32), key);
+    uint64_t M = (uint64_t)word_of(w, i & 3u) * s;
     for (uint32_t a = 1; (uint32_t)M < t; ++a) {
-        w = philox4x32_10(make_uint4((uint32_t)P, (uint32_t)(P >> 32), a, TAG_FY32_RETRY), key);
+        w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), i, TAG_FY32_RETRY | (a << 8)), key);
         M = (uint64_t)w.x * s;
     }
     return (uint32_t)(M >> 32);
 }
 
 // D5 for a single step (off the hot loops).
-__device__ __forceinline__ uint32_t fy_draw(PhiloxKey key, uint64_t P, uint32_t s) {
-    if (s > 65536u) return fy32_draw(key, P, s);
-    const uint4 w = fy16_group_words(key, P >> 3);
-    return fy16_from_lane(lane16(w, (uint32_t)(P & 7u)), key, P, s);
+__device__ __forceinline__ uint32_t fy_draw(PhiloxKey key, uint64_t q, uint32_t i) {
+    if (i >= 65536u) return fy32_draw(key, q, i);
+    const uint4 w = fy16_group_words(key, q, i >> 3);
+    return fy16_from_lane(lane16(w, i & 7u), key, q, i);
 }
 
 }  // namespace shuf

@@ -32,16 +32,16 @@ def test_raw_bucket_draws(k, level, p0):
 def test_raw_fy_draws_including_forced_retries():
     K = oracle.problem_key(11, 2)
     rng = np.random.default_rng(5)
-    P = np.concatenate([np.arange(3000), rng.integers(0, 2**50, size=3000)]).astype(np.uint64)
-    s = np.concatenate([np.arange(2, 3002), rng.integers(2, 2**32, size=2000), np.full(1000, 2**31 + 1)])
-    s = s.astype(np.uint32)
-    out = torch.empty(P.shape[0], dtype=torch.int32, device="cuda")
-    shuf.shuf_debug_fy_draws(K, to_dev(P), to_dev(s), out)
+    q = np.concatenate([np.zeros(3000), rng.integers(0, 2**50, size=3000), np.full(300, 12345)]).astype(np.uint64)
+    i = np.concatenate([np.arange(1, 3001), rng.integers(1, 2**32 - 1, size=2000), rng.integers(1, 65536, size=1000),
+                        np.arange(39900, 40200)]).astype(np.uint32)
+    out = torch.empty(q.shape[0], dtype=torch.int32, device="cuda")
+    shuf.shuf_debug_fy_draws(K, to_dev(q), to_dev(i), out)
     got = out.cpu().numpy().view(np.uint32)
-    exp = oracle.fy_draws(K, P, s)
+    exp = oracle.fy_draws(K, q, i)
     assert (got == exp).all()
-    # the s = 2^31+1 block rejects about half of its primary words
-    assert sum(oracle.fy_draw(K, int(p), 2**31 + 1)[1] > 0 for p in P[-1000:]) > 300
+    # s = i+1 near 40000 rejects ~39% of the 16-bit lanes; huge s rejects often too
+    assert sum(oracle.fy_draw(K, int(a), int(b))[1] > 0 for a, b in zip(q[-300:], i[-300:])) > 60
 
 
 # ------------------------------------------------------- end to end ------
