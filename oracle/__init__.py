@@ -84,6 +84,8 @@ def lib():
         L.oracle_shuffle.restype = i32
         L.oracle_segmented.argtypes = [vp, vp, u64, u32, u32, u32, u64, u32, i32, vp]
         L.oracle_segmented.restype = i32
+        L.oracle_points.argtypes = [u64, u32, u32, u64, vp, u64, vp]
+        L.oracle_points.restype = i32
         _lib = L
     return _lib
 
@@ -186,3 +188,16 @@ def segmented(data: np.ndarray, offsets, k: int, L: int, seed: int, max_levels: 
     if rc:
         raise RuntimeError(f"oracle_segmented failed with status {rc}")
     return (a, st.as_dict()) if stats else a
+
+
+def points(n: int, k: int, L: int, seed: int, js) -> np.ndarray:
+    """D6 point queries: pi(j) = input index of the element at output position j
+    of the single shuffle of n elements (key K = seed), for each j in ``js``,
+    without materialising the array (for sampled checks at full size).  For a
+    segment s of a batch pass seed = K(seed, s) and segment-relative j."""
+    j = np.ascontiguousarray(js, dtype=np.uint64)
+    out = np.zeros(j.shape[0], dtype=np.uint64)
+    rc = lib().oracle_points(n, k, L, seed, _ptr(j), j.shape[0], _ptr(out))
+    if rc:
+        raise RuntimeError(f"oracle_points failed with status {rc}")
+    return out

@@ -102,6 +102,23 @@ int oracle_lemire32_accept(uint32_t w, uint32_t s, uint32_t *out)
 }
 
 /* ---------------------------------------------------------------- D4 ---- */
+/* The primary bucket draws of 8 or 16 consecutive positions share one Philox
+ * block; remembering the last block (same key and counter => same output)
+ * only saves recomputation -- results are those of oracle_philox4x32_10.  */
+static void philox_memo(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    static _Thread_local uint32_t mc[4], mk[2], mo[4];
+    static _Thread_local int have = 0;
+    if (!(have && mc[0] == ctr[0] && mc[1] == ctr[1] && mc[2] == ctr[2] && mc[3] == ctr[3] && mk[0] == key[0] &&
+          mk[1] == key[1])) {
+        oracle_philox4x32_10(ctr, key, mo);
+        memcpy(mc, ctr, sizeof mc);
+        memcpy(mk, key, sizeof mk);
+        have = 1;
+    }
+    memcpy(out, mo, sizeof mo);
+}
+
 #define TAG_SC 1u
 #define TAG_FY16 2u
 #define TAG_SC_RETRY 3u
@@ -136,7 +153,7 @@ uint32_t oracle_bucket_draw(uint64_t K, uint32_t level, uint64_t p, uint32_t k, 
         ctr[1] = (uint32_t)(g >> 32);
         ctr[2] = level;
         ctr[3] = TAG_SC;
-        oracle_philox4x32_10(ctr, key, w);
+        philox_memo(ctr, key, w);
         uint32_t j = (uint32_t)(p & 15u);
         uint32_t v = (w[j >> 2] >> (8u * (j & 3u))) & 0xFFu;
         return v >> (8 - b);
@@ -146,7 +163,7 @@ uint32_t oracle_bucket_draw(uint64_t K, uint32_t level, uint64_t p, uint32_t k, 
     ctr[1] = (uint32_t)(g >> 32);
     ctr[2] = level;
     ctr[3] = TAG_SC;
-    oracle_philox4x32_10(ctr, key, w);
+    philox_memo(ctr, key, w);
     uint32_t j = (uint32_t)(p & 7u);
     uint32_t v = (w[j >> 1] >> (16u * (j & 1u))) & 0xFFFFu;
     if (oracle_lemire16_accept(v, k, &out))
@@ -419,5 +436,176 @@ int oracle_segmented(void *data, const uint64_t *offsets, uint64_t num_segments,
     }
     free(c.T);
     free(c.ids);
+    return rc;
+}
+
+/* ------------------------------------------------- D6 point queries ---- */
+/* pi(j) for selected output positions j of the single shuffle D6 (key
+ * K = seed), without materialising the n-element array: the recursion of D6
+ * is walked only into the segments that contain a queried position.  Used to
+ * check the GPU output at BASELINE.json's full sizes on sampled positions.
+ *
+ * In segment [a, a+m) at level l (m > L): c_b and o_b exactly as D6; the
+ * output position j lies in child b with o_b <= j < o_b + c_b; after the
+ * child has resolved j to a position x of the child's INPUT range (= this
+ * level's output range), the element there is the (x - o_b)-th element, in
+ * ascending i, of bucket b of this segment's input (stability):
+ * one pass over i finds it.  A leaf (m <= L) runs Fig. 1 on the index array
+ * 0..m-1 with the D5 draws of leaf id a, and x = a + idx[j - a].            */
+typedef struct {
+    uint64_t j;     /* queried output position                              */
+    uint64_t x;     /* resolved position in the current segment's input     */
+    uint32_t b;     /* child bucket at the current level                    */
+    uint32_t pad;
+    uint64_t r;     /* rank of x within child b                             */
+} oq_t;
+
+typedef struct {
+    uint64_t K;
+    uint32_t k, L;
+    /* one-group memo of the last Philox call, so a pass over a range costs
+     * one generator call per group like the definition's lane layout       */
+    uint32_t level;
+    uint64_t g;
+    int have;
+} oq_ctx;
+
+static uint32_t oq_bucket(oq_ctx *c, uint32_t level, uint64_t p)
+{
+    /* plain D4 (oracle_bucket_draw), evaluated position by position */
+    (void)c;
+    return oracle_bucket_draw(c->K, level, p, c->k, NULL);
+}
+
+static int oq_cmp_br(const void *x, const void *y)
+{
+    const oq_t *a = *(const oq_t *const *)x, *b = *(const oq_t *const *)y;
+    if (a->b != b->b)
+        return a->b < b->b ? -1 : 1;
+    if (a->r != b->r)
+        return a->r < b->r ? -1 : 1;
+    return 0;
+}
+
+/* resolve every query of q[0..nq) (all inside [a, a+m)) to x = input position */
+static int oq_rec(oq_ctx *c, uint64_t a, uint64_t m, uint32_t level, oq_t **q, uint64_t nq)
+{
+    if (nq == 0)
+        return 0;
+    if (m <= c->L) { /* leaf: Fig. 1 on indices */
+        uint32_t *idx = (uint32_t *)malloc((m ? m : 1) * sizeof(uint32_t));
+        if (!idx)
+            return ORACLE_ERR_NOMEM;
+        for (uint64_t t = 0; t < m; t++)
+            idx[t] = (uint32_t)t;
+        for (uint64_t i = m; i-- > 1;) {
+            uint32_t jj = oracle_fy_draw(c->K, a, (uint32_t)i, NULL);
+            uint32_t tmp = idx[i];
+            idx[i] = idx[jj];
+            idx[jj] = tmp;
+        }
+        for (uint64_t s = 0; s < nq; s++)
+            q[s]->x = a + idx[q[s]->j - a];
+        free(idx);
+        return 0;
+    }
+    if (level > 255)
+        return ORACLE_ERR_DEPTH;
+    uint32_t k = c->k;
+    uint64_t *cnt = (uint64_t *)calloc(k, sizeof(uint64_t));
+    uint64_t *o = (uint64_t *)malloc(k * sizeof(uint64_t));
+    oq_t **tmpq = (oq_t **)malloc(nq * sizeof(oq_t *));
+    uint64_t *ptr = (uint64_t *)malloc((k + 1) * sizeof(uint64_t));
+    uint32_t *lb = (uint32_t *)malloc(nq * sizeof(uint32_t)); /* this level's child of each query */
+    if (!cnt || !o || !tmpq || !ptr || !lb) {
+        free(cnt); free(o); free(tmpq); free(ptr); free(lb);
+        return ORACLE_ERR_NOMEM;
+    }
+    for (uint64_t i = 0; i < m; i++)
+        cnt[oq_bucket(c, level, a + i)]++;
+    uint64_t acc = a;
+    for (uint32_t b = 0; b < k; b++) {
+        o[b] = acc;
+        acc += cnt[b];
+    }
+    /* child of every query: largest b with o_b <= j and c_b > 0 */
+    for (uint64_t s = 0; s < nq; s++) {
+        uint32_t b = 0;
+        for (uint32_t bb = 0; bb < k; bb++)
+            if (cnt[bb] > 0 && o[bb] <= q[s]->j)
+                b = bb;
+        lb[s] = b;
+    }
+    /* recurse child by child (queries grouped by child) */
+    int rc = 0;
+    for (uint32_t b = 0; b < k && rc == 0; b++) {
+        uint64_t nb = 0;
+        for (uint64_t s = 0; s < nq; s++)
+            if (lb[s] == b)
+                tmpq[nb++] = q[s];
+        if (nb)
+            rc = oq_rec(c, o[b], cnt[b], level + 1, tmpq, nb);
+    }
+    if (rc == 0) {
+        /* x is now a position of this level's output range, in child b */
+        for (uint64_t s = 0; s < nq; s++) {
+            q[s]->b = lb[s];
+            q[s]->r = q[s]->x - o[lb[s]];
+            tmpq[s] = q[s];
+        }
+        qsort(tmpq, nq, sizeof(oq_t *), oq_cmp_br);
+        /* ptr[b] = first query of bucket b in the sorted list */
+        uint64_t s = 0;
+        for (uint32_t b = 0; b <= k; b++) {
+            while (s < nq && tmpq[s]->b < b)
+                s++;
+            ptr[b] = s;
+        }
+        uint64_t *seen = cnt; /* reuse: occurrences of bucket b so far */
+        memset(seen, 0, k * sizeof(uint64_t));
+        for (uint64_t i = 0; i < m; i++) {
+            uint32_t b = oq_bucket(c, level, a + i);
+            while (ptr[b] < nq && tmpq[ptr[b]]->b == b && tmpq[ptr[b]]->r == seen[b]) {
+                tmpq[ptr[b]]->x = a + i; /* the r-th element of bucket b (stable) */
+                ptr[b]++;
+            }
+            seen[b]++;
+        }
+    }
+    free(cnt); free(o); free(tmpq); free(ptr); free(lb);
+    return rc;
+}
+
+int oracle_points(uint64_t n, uint32_t k, uint32_t L, uint64_t seed, const uint64_t *js, uint64_t count,
+                  uint64_t *out)
+{
+    int rc = check_args(1, k, L);
+    if (rc)
+        return rc;
+    if (count == 0)
+        return 0;
+    oq_t *qs = (oq_t *)calloc(count, sizeof(oq_t));
+    oq_t **qp = (oq_t **)malloc(count * sizeof(oq_t *));
+    if (!qs || !qp) {
+        free(qs); free(qp);
+        return ORACLE_ERR_NOMEM;
+    }
+    for (uint64_t s = 0; s < count; s++) {
+        if (js[s] >= n) {
+            free(qs); free(qp);
+            return ORACLE_ERR_INVALID_ARG;
+        }
+        qs[s].j = js[s];
+        qp[s] = &qs[s];
+    }
+    oq_ctx c;
+    memset(&c, 0, sizeof c);
+    c.K = oracle_problem_key(seed, 0);
+    c.k = k;
+    c.L = L;
+    rc = oq_rec(&c, 0, n, 0, qp, count);
+    for (uint64_t s = 0; rc == 0 && s < count; s++)
+        out[s] = qs[s].x;
+    free(qs); free(qp);
     return rc;
 }

@@ -33,4 +33,7 @@ int oracle_shuffle(void *data, uint64_t n, uint32_t eb, uint32_t k, uint32_t L, 
 int oracle_segmented(void *data, const uint64_t *offsets, uint64_t num_segments, uint32_t eb, uint32_t k,
                      uint32_t L, uint64_t seed, uint32_t max_levels, int run_leaves, oracle_stats *st);
 
+int oracle_points(uint64_t n, uint32_t k, uint32_t L, uint64_t seed, const uint64_t *js, uint64_t count,
+                  uint64_t *out);
+
 #endif

@@ -249,7 +249,8 @@ __device__ __forceinline__ void smem_level(const RunParams& rp, const Fin& F, co
 #pragma unroll 4
             for (uint32_t o = 0; o < q; o += 32) {
                 const bool valid = o < lim;
-                const uint32_t b = dp[valid ? o : 0u];
+                // an invalid lane may sit past the draws of this range: force bucket 0
+                const uint32_t b = valid ? (uint32_t)dp[o] : 0u;
                 atomicAdd(&Cw[b >> 1], valid ? (1u << ((b & 1u) << 4)) : 0u);
             }
         }
@@ -269,10 +270,10 @@ __device__ __forceinline__ void smem_level(const RunParams& rp, const Fin& F, co
 #pragma unroll 4
             for (uint32_t o = 0; o < q; o += 32) {
                 const bool valid = o < lim;
-                const uint32_t oo = valid ? o : 0u;
-                const uint32_t b = dp[oo];
+                const uint32_t b = valid ? (uint32_t)dp[o] : 0u;
                 const uint32_t sh = (b & 1u) << 4;
-                const E x = sp[oo];
+                // predicated: an invalid lane's address may lie past the shared window
+                const E x = valid ? sp[o] : E{};
                 const uint32_t slot = (atomicAdd(&Cw[b >> 1], valid ? (1u << sh) : 0u) >> sh) & 0xFFFFu;
                 if (valid) D0[slot] = x;
             }

@@ -113,3 +113,27 @@ def test_repeat_runs_identical_and_stream_independent():
         r2 = gpu_shuffle(a, 256, 4096, 42)
     assert (r1 == r2).all()
     assert (np.sort(r1) == a).all()
+
+
+def test_documented_match_rank_path_bit_exact():
+    """The ranking fallback (__match_any_sync, SHUF_RANK_MODE=match) is chosen
+    once per process, so it runs in a subprocess over every path: HBM levels,
+    shared-memory levels (narrow and wide draws), deep recursion, leaves."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, oracle, paper_2302_03317_b200 as shuf\n"
+        "from tests.gpu_util import gpu_shuffle\n"
+        "cases = [(100_003, 256, 4096, 5), (777_777, 7, 300, 6), (200_000, 2, 1, 8), (3_000_000, 256, 4096, 11),\n"
+        "         (300_001, 1000, 50, 7)]\n"
+        "for n, k, L, seed in cases:\n"
+        "    a = np.arange(n, dtype=np.uint32)\n"
+        "    assert (gpu_shuffle(a, k, L, seed) == oracle.shuffle(a, k, L, seed)).all(), (n, k, L, seed)\n"
+        "assert shuf.lib().shuf_rank_mode() == 0\n"
+        "print('ok')\n" % root)
+    env = dict(os.environ, SHUF_RANK_MODE="match")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

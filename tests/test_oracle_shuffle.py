@@ -209,3 +209,14 @@ def test_oracle_matches_independent_numpy_derivation(n, k, L, seed):
     got = oracle.shuffle(a, k, L, seed)
     exp = shuffle_np(a, k, L, oracle.problem_key(seed, 0))
     assert (got == exp).all()
+
+
+@pytest.mark.parametrize("n,k,L,seed", [(1, 2, 1, 1), (2, 2, 1, 1), (37, 2, 1, 2), (5000, 7, 30, 3),
+                                        (100_003, 256, 300, 5), (300_001, 1000, 50, 7), (200_000, 2, 1, 8),
+                                        (1 << 20, 256, 4096, 1)])
+def test_point_queries_equal_full_shuffle(n, k, L, seed):
+    """oracle.points (the D6 walk used for sampled checks at full size) resolves
+    every queried output position to the same input index as the full D6."""
+    pi = oracle.shuffle(np.arange(n, dtype=np.uint64), k, L, seed)
+    js = np.arange(n, dtype=np.uint64) if n <= 5000 else np.random.default_rng(seed).integers(0, n, 300).astype(np.uint64)
+    assert (oracle.points(n, k, L, seed, js) == pi[js.astype(np.int64)]).all()
