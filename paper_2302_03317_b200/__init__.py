@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "shuf_plan", "shuf_last_status", "shuf_scratch_bytes", "shuf_run", "shuf_segmented", "shuf_debug_run_levels",
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
-    "shuf_last_run_stats", "shuf_rank_mode",
+    "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish"]
 
@@ -86,6 +86,8 @@ def lib():
         L.shuf_profile_run.restype = i32
         L.shuf_last_run_stats.argtypes = [vp, vp, vp, u32]
         L.shuf_last_run_stats.restype = i32
+        L.shuf_debug_clocks.argtypes = [vp, vp, vp, u32]
+        L.shuf_debug_clocks.restype = i32
         L.shuf_rank_mode.restype = i32
         L.shuf_status_string.argtypes = [i32]
         L.shuf_status_string.restype = ctypes.c_char_p
@@ -226,6 +228,13 @@ def shuf_last_run_stats(plan: Plan, stream=None) -> dict:
     sm = [int(buf[3 + 2 * l]) for l in range(256)]
     top = max([l + 1 for l in range(256) if hbm[l] or sm[l]] or [0])
     return {"finished": int(buf[0]), "fy_elems": int(buf[1]), "scattered_hbm": hbm[:top], "scattered_smem": sm[:top]}
+
+
+def shuf_debug_clocks(plan: Plan, stream=None) -> list:
+    """Phase clocks of CTA 0 of the fast finish in the last run (6 per item)."""
+    buf = (ctypes.c_longlong * 256)()
+    _check(lib().shuf_debug_clocks(plan.handle, _stream(stream), buf, 256), "shuf_debug_clocks", plan)
+    return [int(buf[i]) for i in range(256)]
 
 
 def shuf_destroy(plan: Plan):

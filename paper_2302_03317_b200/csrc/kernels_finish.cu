@@ -470,6 +470,8 @@ struct ChildIter {
                 const uint64_t s0 = ctl->ub[b - b0], len = ctl->ub[b - b0 + 1] - s0;
                 if (len == 0 || len > rp->S_fuse) continue;
                 if (lp->dst == rp->buf0 && !item_permutes(*rp, (uint32_t)len, lvl)) continue;
+                // children finished by k_finish_fast carry flag 0
+                if (rp->fast && rp->flags[(ctl->u / groups) * rp->k + b] == 0) continue;
                 __syncwarp();
                 if (lane == 0) {
                     Item& it = ctl->items[slot];

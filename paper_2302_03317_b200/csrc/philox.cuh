@@ -83,7 +83,7 @@ __device__ __forceinline__ uint4 bucket_group_words(PhiloxKey key, uint32_t leve
 }
 
 // Slow path of D4 (wide, non-power-of-two k): retry stream.
-static __device__ __noinline__ uint32_t bucket_retry(PhiloxKey key, uint32_t level, uint64_t p, uint32_t k,
+__device__ __forceinline__ uint32_t bucket_retry(PhiloxKey key, uint32_t level, uint64_t p, uint32_t k,
                                                      uint32_t t) {
     for (uint32_t a = 1;; ++a) {
         uint4 w = philox4x32_10(make_uint4((uint32_t)p, (uint32_t)(p >> 32), level | (a << 8), TAG_SC_RETRY), key);
@@ -126,7 +126,7 @@ __device__ __forceinline__ uint4 fy16_group_words(PhiloxKey key, uint64_t q, uin
     return philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), grp, TAG_FY16), key);
 }
 
-static __device__ __noinline__ uint32_t fy16_retry(PhiloxKey key, uint64_t q, uint32_t i) {
+__device__ __forceinline__ uint32_t fy16_retry(PhiloxKey key, uint64_t q, uint32_t i) {
     const uint32_t s = i + 1, t = 65536u % s;
     for (uint32_t a = 1;; ++a) {
         uint4 w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), i, TAG_FY16_RETRY | (a << 8)), key);

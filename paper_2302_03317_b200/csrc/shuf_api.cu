@@ -27,7 +27,8 @@ struct shuf_plan_s {
     // device setup (lazily, first run)
     bool dev_ready;
     int sms;
-    int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small;
+    int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small, grid_fast;
+    int fast;
     int rank_ordered;
     uint32_t finish_smem, scatter_smem;
     int last_cuda_error;
@@ -105,6 +106,8 @@ static void compute_layout(shuf_plan_s* p) {
         l.status[s] = off;
         off = align_up(off + l.max_tiles * 8, 256);
     }
+    l.flags = off;
+    off = align_up(off + l.max_segs * p->k, 256);
     l.total = off;
 }
 
@@ -212,6 +215,16 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     p->scatter_smem = scatter_smem_bytes(p->eb, p->k);
     if ((e = configure_finish(p->finish_smem))) return e;
     if ((e = configure_scatter(p->scatter_smem))) return e;
+    // fast finish (kernels_fast.cu, experimental): ordered-atomic ranking only;
+    // SHUF_FAST_FINISH=1 enables it
+    {
+        const char* ff = std::getenv("SHUF_FAST_FINISH");
+        p->fast = (p->rank_ordered && p->k <= kMaxK && (ff && ff[0] == '1') &&
+                   fast_smem_bytes(p->eb, p->k) <= kSmemLimit)
+                      ? 1
+                      : 0;
+        if (p->fast && (e = configure_fast(p->eb, p->k))) return e;
+    }
     // persistent grids: SM count x resident CTAs per SM
     int oh = 1, os = 1, osc = 1, of = 1;
     if ((e = occupancy_level(p->eb, p->k, &oh, &os, &osc))) return e;
@@ -222,6 +235,7 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     p->grid_scatter = p->sms * clamp1(osc);
     p->grid_finish = p->sms * clamp1(of);
     p->grid_small = p->sms * 4;
+    p->grid_fast = p->sms;
     p->dev_ready = true;
     return cudaSuccess;
 }
@@ -311,6 +325,8 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     rp.seed = p->seed;
     rp.rank_ordered = (uint32_t)p->rank_ordered;
     rp.fin_nbuf = p->fin_nbuf;
+    rp.fast = (uint32_t)p->fast;
+    rp.flags = sc + p->lay.flags;
     uint64_t launches = 0;
     if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
     const LevelParams lp0 = level_params(p, sc, buf0, 0);
@@ -328,6 +344,7 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         LAUNCH(SHUF_K_SCAN, launch_scan(rp, lp, st, p->grid_scan));
         LAUNCH(SHUF_K_PLAN, launch_plan(rp, lp, st, p->grid_small));
         LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
+        if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast(rp, lp, st, p->grid_fast));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
         if (lv + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
     }
@@ -454,4 +471,15 @@ extern "C" const char* shuf_status_string(shuf_status s) {
     case SHUF_ERR_CUDA: return "CUDA error";
     }
     return "unknown status";
+}
+
+// Debug: phase clocks recorded by CTA 0 of the fast finish (kernels_fast.cu).
+extern "C" shuf_status shuf_debug_clocks(shuf_plan_t p, void* stream, long long* out, uint32_t count) {
+    if (!p || !out) return SHUF_ERR_INVALID_ARG;
+    if (!p->last_hdr) return SHUF_OK;
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e) return cuda_fail(p, e);
+    if (count > 256) count = 256;
+    if ((e = cudaMemcpy(out, p->last_hdr->clk, count * sizeof(long long), cudaMemcpyDeviceToHost))) return cuda_fail(p, e);
+    return SHUF_OK;
 }

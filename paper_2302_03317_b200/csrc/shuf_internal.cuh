@@ -56,6 +56,7 @@ struct Header {
     uint64_t scattered_smem[kMaxLevels];  // elements scattered in shared memory at level l
     uint64_t finished;                    // elements written by the fused finish
     uint64_t fy_elems;                    // elements in Fisher-Yates leaves
+    long long clk[256];                   // phase timestamps of CTA 0 of the fast finish (shuf_debug_clocks)
 };
 
 // Byte offsets of every region inside the caller's scratch buffer.
@@ -67,6 +68,7 @@ struct ScratchLayout {
     uint64_t counts[2];  // u32 per (bucket, chunk)
     uint64_t prefix[2];  // u64 per (bucket, chunk)
     uint64_t status[2];  // u64 per scan tile
+    uint64_t flags;      // u8 per child of a level: 1 = finished by the general finish kernel
     uint64_t total;
     uint64_t max_segs, max_chunks, max_entries, max_tiles;
 };
@@ -89,6 +91,8 @@ struct RunParams {
     uint64_t seed;
     uint32_t rank_ordered;  // 1: ordered shared atomics verified on this GPU (block_ops.cuh)
     uint32_t fin_nbuf;      // finish-kernel data buffers (2 = items double-buffered)
+    uint32_t fast;          // 1: k_finish_fast runs first; the general finish takes flagged children only
+    unsigned char* flags;   // per-child flags of the current level (ScratchLayout::flags)
 };
 
 struct LevelParams {
@@ -123,6 +127,10 @@ cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offset
 uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t nbuf);
 uint32_t finish_max_elems(uint32_t eb, uint32_t k);
 uint32_t finish_smem_budget(uint32_t eb);
+cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t configure_fast(uint32_t eb, uint32_t k);
+uint32_t fast_smem_bytes(uint32_t eb, uint32_t k);
+uint32_t fast_max_elems(uint32_t eb);
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);

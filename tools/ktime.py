@@ -1,0 +1,43 @@
+"""Per-kernel-class CUDA-event times of one warm shuffle (shuf_profile_run).
+usage: python tools/ktime.py [workload] [reps]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2302_03317_b200 as shuf  # noqa: E402
+import synth  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "hot"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+w = synth.WORKLOADS[wl]
+dev = torch.device("cuda", 0)
+x = synth.make_input_torch(w, dev)
+plan = shuf.shuf_plan(w.n, w.elem_bytes, w.k, w.L, w.seed)
+scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
+for _ in range(2):
+    shuf.shuf_run(plan, x, scratch)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(reps):
+    shuf.shuf_run(plan, x, scratch)
+e1.record()
+torch.cuda.synchronize()
+print(f"{wl}: {e0.elapsed_time(e1) / reps:.3f} ms/shuffle (stream-ordered, no per-launch events)")
+prof = shuf.shuf_profile_run(plan, x, scratch, None)
+for k, (ms, n) in prof.items():
+    print(f"  {k:8s} {ms:8.3f} ms  launches={n}")
+print("device error", shuf.shuf_last_device_error(plan))
+shuf.shuf_run(plan, x, scratch)
+c = shuf.shuf_debug_clocks(plan)
+print("fast-finish CTA 0 phase clocks per item (cycles from the start of phase A)")
+for it in range(1, 12):
+    a0, fy, dc, sc, pl, pa = c[it * 6: it * 6 + 6]
+    if a0 == 0:
+        break
+    nxt = c[(it + 1) * 6]
+    print(f"  item {it}: draw+count {dc - a0:6d}  fy_end {fy - a0:6d}  scan_end {sc - a0:6d}"
+          f"  place_end {pl - a0:6d}  partners_end {pa - a0:6d}  total {nxt - a0 if nxt else 0:6d}")
