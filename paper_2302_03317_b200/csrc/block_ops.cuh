@@ -167,4 +167,27 @@ __device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t
     __syncthreads();
 }
 
+// As scan_counters for unpacked u32 counters: C holds nw tables of k words
+// (table w at C + w*k).
+template <int NT>
+__device__ __forceinline__ void scan_counters32(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum) {
+    const uint32_t per = (k + NT - 1) / NT;
+    const uint32_t x0 = threadIdx.x * per, x1 = min(k, x0 + per);
+    uint32_t mine = 0;
+    for (uint32_t x = x0; x < x1; ++x)
+        for (uint32_t w = 0; w < nw; ++w) mine += C[w * k + x];
+    uint32_t total;
+    uint32_t run = block_exclusive_sum<NT>(mine, wsum, &total);
+    for (uint32_t x = x0; x < x1; ++x) {
+        bst[x] = run;
+        for (uint32_t w = 0; w < nw; ++w) {
+            const uint32_t c = C[w * k + x];
+            C[w * k + x] = run;
+            run += c;
+        }
+    }
+    if (threadIdx.x == 0) bst[k] = total;
+    __syncthreads();
+}
+
 }  // namespace shuf

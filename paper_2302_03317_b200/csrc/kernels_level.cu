@@ -1,5 +1,5 @@
 // HBM-resident ("global") scatter level: init, histogram, decoupled-lookback
-// scan, segment planner and the TMA-staged stable scatter.
+// scan and segment planner (the stable scatter itself: kernels_scatter.cu).
 //
 // One level l over the active segments computes, for every segment s of
 // length m at [a, a+m) (D6, P:140-142 with pi stable):
@@ -269,243 +269,6 @@ __global__ void k_plan(RunParams rp, LevelParams lp) {
     }
 }
 
-// ---------------------------------------------------------------- scatter --
-// Per CTA: a sequence of tiles (chunks blockIdx.x, +gridDim.x, ..., each walked
-// tile by tile in order).  Tile t lands in buffer t&1 by one bulk async copy
-// issued while tile t-1 is processed.  Each warp loads its 32-element rounds
-// into registers and ranks them (block_ops.cuh); the (bucket, warp) counters
-// are scanned into tile-local bases; the elements are written back into the
-// same buffer in bucket-major stable order together with their bucket byte;
-// then every thread copies slots s = tid, tid+512, ... to
-// dst[running[b] - bst[b] + s] (consecutive lanes -> consecutive addresses
-// inside a bucket run).
-template <int EB>
-struct ScatterCfg {
-    static constexpr uint32_t T = 32768 / EB;       // elements per tile (32 KiB)
-    static constexpr uint32_t Q = T / kWarps;        // elements per warp
-    static constexpr uint32_t R = Q / 32;            // rounds per warp
-    static constexpr uint32_t BUF = T * EB + 16;
-};
-
-struct ScatterLayout {
-    uint32_t buf0, buf1, draws, slotb, C, bst, delta, running, wsum, bar, total;
-};
-
-template <int EB>
-__host__ __device__ inline ScatterLayout scatter_layout(uint32_t k) {
-    ScatterLayout L;
-    uint32_t off = 0;
-    auto take = [&off](uint32_t bytes) {
-        const uint32_t at = off;
-        off = (off + bytes + 15u) & ~15u;
-        return at;
-    };
-    constexpr uint32_t T = ScatterCfg<EB>::T;
-    L.buf0 = take(ScatterCfg<EB>::BUF);
-    L.buf1 = take(ScatterCfg<EB>::BUF);
-    L.draws = take(draw_bytes(T));
-    const bool narrow = (k & (k - 1)) == 0 && k <= 256;  // u8 bucket ids (make_bucket_params)
-    L.slotb = take(narrow ? T : 2 * T);
-    L.C = take(kWarps * ((k + 1) / 2) * 4);
-    L.bst = take((k + 1) * 4);
-    L.delta = take(k * 8);
-    L.running = take(k * 8);
-    L.wsum = take((kWarps + 1) * 4);
-    L.bar = take(16);
-    L.total = off;
-    return L;
-}
-
-struct TileRef {
-    uint32_t chunk;   // chunk index (>= nchunk: none)
-    uint32_t seg;     // segment index
-    uint64_t q0, q1;  // element range of the chunk's remaining part
-};
-
-__device__ __forceinline__ TileRef first_tile(const LevelParams& lp, const RunParams& rp, uint32_t j, uint32_t nchunk) {
-    TileRef t;
-    t.chunk = j;
-    t.seg = 0;
-    t.q0 = t.q1 = 0;
-    if (j >= nchunk) return t;
-    const ChunkDesc ch = lp.chunks[j];
-    const SegDesc& sg = lp.segs[ch.seg];
-    t.seg = ch.seg;
-    t.q0 = sg.start + (uint64_t)ch.c * rp.chunk;
-    t.q1 = min(sg.start + sg.len, t.q0 + rp.chunk);
-    return t;
-}
-
-template <int EB>
-__device__ __forceinline__ void issue_tile_load(uint64_t q0, uint32_t cnt, const unsigned char* src,
-                                                unsigned char* buf, uint64_t* bar) {
-    const uint32_t tid = threadIdx.x;
-    const uint64_t x0 = q0 * EB, x1 = (q0 + cnt) * EB;
-    const uint64_t fl = x0 & ~15ull;
-    const uint64_t A = (x0 + 15) & ~15ull, B = x1 & ~15ull;
-    const bool body = B > A;
-    if (tid == 0) {
-        fence_proxy_async();
-        mbar_arrive_expect_tx(bar, body ? (uint32_t)(B - A) : 0u);
-        if (body) bulk_g2s(buf + (A - fl), src + A, (uint32_t)(B - A), bar);
-    }
-    const uint64_t hEnd = body ? A : x1;
-    const uint32_t nh = (uint32_t)((hEnd - x0) >> 2);
-    const uint64_t tBeg = body ? B : x1;
-    const uint32_t nt = (uint32_t)((x1 - tBeg) >> 2);
-    if (tid >= 32 && tid - 32 < nh)
-        *reinterpret_cast<uint32_t*>(buf + (x0 - fl) + 4 * (tid - 32)) =
-            *reinterpret_cast<const uint32_t*>(src + x0 + 4 * (tid - 32));
-    else if (tid >= 64 && tid - 64 < nt)
-        *reinterpret_cast<uint32_t*>(buf + (tBeg - fl) + 4 * (tid - 64)) =
-            *reinterpret_cast<const uint32_t*>(src + tBeg + 4 * (tid - 64));
-}
-
-template <bool ORD>
-__device__ __forceinline__ uint32_t rank_in_warp(uint32_t* Cw, uint32_t b, bool valid) {
-    if (ORD) {
-        const uint32_t sh = (b & 1u) << 4;
-        const uint32_t old = valid ? atomicAdd(&Cw[b >> 1], 1u << sh) : 0u;
-        return (old >> sh) & 0xFFFFu;
-    } else {
-        return warp_rank(Cw, b, valid, false);
-    }
-}
-
-// Rank + place one tile (FULL: cnt == T, no bounds checks).
-template <int EB, bool ORD, bool NARROW, bool FULL>
-__device__ __forceinline__ void rank_place(unsigned char* buf, uint32_t in_off, uint32_t cnt, const DrawView& dv,
-                                           uint32_t* C, uint32_t kw, uint32_t k, uint32_t* bst, uint32_t* wsum,
-                                           unsigned char* slotb) {
-    using E = typename ElemT<EB>::type;
-    constexpr uint32_t Q = ScatterCfg<EB>::Q, R = ScatterCfg<EB>::R;
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const unsigned char* tin = buf + in_off;
-    uint32_t* Cw = C + warp * kw;
-    E v[R];
-    uint32_t rk[R];
-#pragma unroll
-    for (uint32_t r = 0; r < R; ++r) {
-        const uint32_t e = warp * Q + r * 32 + lane;
-        const bool valid = FULL || e < cnt;
-        uint32_t b = 0;
-        if (valid) {
-            v[r] = *reinterpret_cast<const E*>(tin + e * EB);
-            b = NARROW ? (uint32_t)dv.d[e + dv.off] : (uint32_t)reinterpret_cast<const uint16_t*>(dv.d)[e + dv.off];
-        }
-        rk[r] = (b << 16) | rank_in_warp<ORD>(Cw, b, valid);
-    }
-    __syncthreads();
-    scan_counters<kThreads>(C, kWarps, k, bst, wsum);
-    E* stage = reinterpret_cast<E*>(buf);
-#pragma unroll
-    for (uint32_t r = 0; r < R; ++r) {
-        const uint32_t e = warp * Q + r * 32 + lane;
-        if (FULL || e < cnt) {
-            const uint32_t b = rk[r] >> 16;
-            const uint32_t slot = ((Cw[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu) + (rk[r] & 0xFFFFu);
-            stage[slot] = v[r];
-            if (NARROW) slotb[slot] = (unsigned char)b;
-            else reinterpret_cast<uint16_t*>(slotb)[slot] = (uint16_t)b;
-        }
-    }
-}
-
-template <int EB, bool ORD, bool NARROW>
-__global__ void __launch_bounds__(kThreads, 2) k_scatter(RunParams rp, LevelParams lp) {
-    using E = typename ElemT<EB>::type;
-    constexpr uint32_t T = ScatterCfg<EB>::T;
-    extern __shared__ __align__(16) unsigned char sm[];
-    const uint32_t k = rp.k, kw = (k + 1) >> 1;
-    const ScatterLayout Ly = scatter_layout<EB>(k);
-    unsigned char* dsm = sm + Ly.draws;
-    unsigned char* slotb = sm + Ly.slotb;
-    uint32_t* C = reinterpret_cast<uint32_t*>(sm + Ly.C);
-    uint32_t* bst = reinterpret_cast<uint32_t*>(sm + Ly.bst);
-    uint64_t* delta = reinterpret_cast<uint64_t*>(sm + Ly.delta);
-    uint64_t* running = reinterpret_cast<uint64_t*>(sm + Ly.running);
-    uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + Ly.wsum);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + Ly.bar);
-
-    const uint32_t tid = threadIdx.x;
-    const uint32_t nchunk = lp.ctr->nchunk;
-    if (blockIdx.x >= nchunk) return;
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const unsigned char* __restrict__ src = lp.src;
-    E* __restrict__ dst = reinterpret_cast<E*>(lp.dst);
-    uint32_t ph0 = 0, ph1 = 0;
-
-    TileRef cur = first_tile(lp, rp, blockIdx.x, nchunk);
-    uint32_t cnt = (uint32_t)min((uint64_t)T, cur.q1 - cur.q0);
-    issue_tile_load<EB>(cur.q0, cnt, src, sm + Ly.buf0, &bar[0]);
-    unsigned long long scattered = cur.q1 - cur.q0;
-    bool new_chunk = true;
-    for (uint32_t it = 0; cur.chunk < nchunk; ++it) {
-        // ---- prefetch the next tile of this CTA's sequence into the other buffer
-        TileRef nxt = cur;
-        nxt.q0 = cur.q0 + cnt;
-        const bool next_chunk = nxt.q0 >= cur.q1;
-        if (next_chunk) {
-            nxt = first_tile(lp, rp, cur.chunk + gridDim.x, nchunk);
-            if (nxt.chunk < nchunk) scattered += nxt.q1 - nxt.q0;
-        }
-        const uint32_t ncnt = (uint32_t)min((uint64_t)T, nxt.q1 - nxt.q0);
-        unsigned char* buf = sm + ((it & 1u) ? Ly.buf1 : Ly.buf0);
-        if (nxt.chunk < nchunk)
-            issue_tile_load<EB>(nxt.q0, ncnt, src, sm + ((it & 1u) ? Ly.buf0 : Ly.buf1), &bar[(it & 1u) ^ 1u]);
-        const SegDesc sg = lp.segs[cur.seg];
-        if (new_chunk) {
-            const ChunkDesc ch = lp.chunks[cur.chunk];
-            const uint64_t base0 = lp.prefix[sg.cbase];
-            for (uint32_t b = tid; b < k; b += kThreads)
-                running[b] = sg.start + lp.prefix[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] - base0;
-        }
-        // ---- draws of the tile's positions, zero the counters, wait for the data
-        const DrawView dv = draws_to_smem<kThreads>(dsm, cur.q0 - sg.origin, cnt, make_key(sg.key), lp.level, rp.bp);
-        for (uint32_t i = tid; i < kWarps * kw; i += kThreads) C[i] = 0;
-        if (it & 1u) {
-            mbar_wait(&bar[1], ph1);
-            ph1 ^= 1u;
-        } else {
-            mbar_wait(&bar[0], ph0);
-            ph0 ^= 1u;
-        }
-        __syncthreads();
-        const uint32_t in_off = (uint32_t)((cur.q0 * EB) & 15u);
-        if (cnt == T) rank_place<EB, ORD, NARROW, true>(buf, in_off, cnt, dv, C, kw, k, bst, wsum, slotb);
-        else rank_place<EB, ORD, NARROW, false>(buf, in_off, cnt, dv, C, kw, k, bst, wsum, slotb);
-        for (uint32_t b = tid; b < k; b += kThreads) {
-            delta[b] = running[b] - bst[b];
-            running[b] += bst[b + 1] - bst[b];
-        }
-        __syncthreads();
-        // ---- copy out: slot s goes to dst[running[b] - bst[b] + s]
-        const E* stage = reinterpret_cast<const E*>(buf);
-        if (cnt == T) {
-#pragma unroll 4
-            for (uint32_t s = tid; s < T; s += kThreads) {
-                const uint32_t b = NARROW ? (uint32_t)slotb[s] : (uint32_t)reinterpret_cast<const uint16_t*>(slotb)[s];
-                dst[delta[b] + s] = stage[s];
-            }
-        } else {
-            for (uint32_t s = tid; s < cnt; s += kThreads) {
-                const uint32_t b = NARROW ? (uint32_t)slotb[s] : (uint32_t)reinterpret_cast<const uint16_t*>(slotb)[s];
-                dst[delta[b] + s] = stage[s];
-            }
-        }
-        __syncthreads();
-        new_chunk = next_chunk;
-        cur = nxt;
-        cnt = ncnt;
-    }
-    if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->scattered_hbm[lp.level], scattered);
-}
-
 // --------------------------------------------------------------- launchers --
 cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid) {
     k_init_single<<<grid, 256, 0, s>>>(rp, lp0);
@@ -533,54 +296,11 @@ cudaError_t launch_plan(const RunParams& rp, const LevelParams& lp, cudaStream_t
     return cudaGetLastError();
 }
 
-uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k) {
-    switch (eb) {
-    case 4: return scatter_layout<4>(k).total;
-    case 8: return scatter_layout<8>(k).total;
-    default: return scatter_layout<16>(k).total;
-    }
-}
-
-// Kernel selection: element size x ranking mode x lane width.
-template <int EB>
-static void* scatter_fn(bool ord, bool narrow) {
-    if (ord) return narrow ? (void*)k_scatter<EB, true, true> : (void*)k_scatter<EB, true, false>;
-    return narrow ? (void*)k_scatter<EB, false, true> : (void*)k_scatter<EB, false, false>;
-}
-
-static void* scatter_kernel(const RunParams& rp) {
-    const bool ord = rp.rank_ordered != 0, nar = rp.bp.narrow != 0;
-    switch (rp.eb) {
-    case 4: return scatter_fn<4>(ord, nar);
-    case 8: return scatter_fn<8>(ord, nar);
-    default: return scatter_fn<16>(ord, nar);
-    }
-}
-
-cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
-    const uint32_t smem = scatter_smem_bytes(rp.eb, rp.k);
-    void* args[] = {(void*)&rp, (void*)&lp};
-    return cudaLaunchKernel(scatter_kernel(rp), dim3(grid), dim3(kThreads), args, smem, s);
-}
-
-cudaError_t configure_scatter(uint32_t smem) {
-    cudaError_t e;
-    for (int eb : {4, 8, 16})
-        for (int o = 0; o < 2; ++o)
-            for (int nr = 0; nr < 2; ++nr) {
-                void* f = eb == 4 ? scatter_fn<4>(o, nr) : (eb == 8 ? scatter_fn<8>(o, nr) : scatter_fn<16>(o, nr));
-                if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-            }
-    return cudaSuccess;
-}
-
 cudaError_t occupancy_level(uint32_t eb, uint32_t k, int* hist, int* scan, int* scatter) {
     cudaError_t e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(hist, k_hist, kThreads, k * sizeof(uint32_t)))) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(scan, k_scan, kThreads, 0))) return e;
-    const uint32_t smem = scatter_smem_bytes(eb, k);
-    void* f = eb == 4 ? scatter_fn<4>(true, true) : (eb == 8 ? scatter_fn<8>(true, true) : scatter_fn<16>(true, true));
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(scatter, f, kThreads, smem);
+    return occupancy_scatter(eb, k, scatter);
 }
 
 }  // namespace shuf

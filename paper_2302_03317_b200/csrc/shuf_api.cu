@@ -143,7 +143,7 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     p->seed = seed;
     p->S_fuse = S;
     p->fin_nbuf = nbuf;
-    const uint32_t T = 32768u / elem_bytes;  // scatter tile (kernels_level.cu ScatterCfg)
+    const uint32_t T = kScatterTileBytes / elem_bytes;  // scatter tile (kernels_scatter.cu SCfg)
     uint64_t C = (n + 16383) / 16384;
     C = align_up(C < T ? T : C, T);
     if (C > 0x40000000ull) C = 0x40000000ull;

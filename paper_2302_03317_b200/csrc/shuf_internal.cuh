@@ -17,6 +17,7 @@ constexpr uint32_t kSmemLimit = 227 * 1024;
 constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
 constexpr uint32_t kSegGroup = 8;          // user segments per finish work unit (segmented mode)
 constexpr uint32_t kMaxLevels = 256;
+constexpr uint32_t kScatterTileBytes = 24576; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
 constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
 
 // ---------------------------------------------------------- descriptors ---
@@ -135,6 +136,7 @@ cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStre
 cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);
 cudaError_t configure_scatter(uint32_t smem);
+cudaError_t occupancy_scatter(uint32_t eb, uint32_t k, int* blocks);
 cudaError_t configure_finish(uint32_t smem);
 cudaError_t occupancy_level(uint32_t eb, uint32_t k, int* hist, int* scan, int* scatter);
 cudaError_t occupancy_finish(uint32_t eb, uint32_t smem, int* blocks);

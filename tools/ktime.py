@@ -10,8 +10,8 @@ import torch  # noqa: E402
 import paper_2302_03317_b200 as shuf  # noqa: E402
 import synth  # noqa: E402
 
-wl = sys.argv[1] if len(sys.argv) > 1 else "hot"
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+wl = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "hot"
+reps = 3
 w = synth.WORKLOADS[wl]
 dev = torch.device("cuda", 0)
 x = synth.make_input_torch(w, dev)
@@ -33,6 +33,15 @@ for k, (ms, n) in prof.items():
 print("device error", shuf.shuf_last_device_error(plan))
 shuf.shuf_run(plan, x, scratch)
 c = shuf.shuf_debug_clocks(plan)
+if "--scatter" in sys.argv:
+    print("scatter CTA 0 level 0 tile phases (cycles): draws+count, wait+sync, scan, place, copyout, total")
+    for it in range(1, 30):
+        t = c[it * 6: it * 6 + 6]
+        if t[0] == 0:
+            break
+        nx = c[(it + 1) * 6]
+        print(f"  tile {it}: {t[1]-t[0]:6d} {t[2]-t[1]:6d} {t[3]-t[2]:6d} {t[4]-t[3]:6d} {t[5]-t[4]:6d}  total {nx - t[0] if nx else 0:6d}")
+    sys.exit(0)
 print("fast-finish CTA 0 phase clocks per item (cycles from the start of phase A)")
 for it in range(1, 12):
     a0, fy, dc, sc, pl, pa = c[it * 6: it * 6 + 6]
