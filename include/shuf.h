@@ -127,9 +127,9 @@ shuf_status shuf_profile_run(shuf_plan_t p, void *ptr, const uint64_t *d_offsets
 shuf_status shuf_last_run_stats(shuf_plan_t p, void *stream, uint64_t *out, uint32_t count);
 
 /* Debug: phase timestamps (clock64) recorded by CTA 0 of the fast finish
- * kernel during the last run on this plan (6 per item: rank phase A start,
- * FY end, draws end, counts end, scan end, placement+prefetch end); writes
- * min(count, 256) values.  Synchronises. */
+ * kernel during the last run on this plan (6 per item) in out[0, 256) and
+ * by CTA 0 of the level-0 HBM scatter (6 per tile) in out[256, 512);
+ * writes min(count, 512) values.  Synchronises. */
 shuf_status shuf_debug_clocks(shuf_plan_t p, void *stream, long long *out, uint32_t count);
 
 /* Synchronise `stream` and return the plan's latched device error (SHUF_OK

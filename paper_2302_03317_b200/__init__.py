@@ -232,9 +232,9 @@ def shuf_last_run_stats(plan: Plan, stream=None) -> dict:
 
 def shuf_debug_clocks(plan: Plan, stream=None) -> list:
     """Phase clocks of CTA 0 of the fast finish in the last run (6 per item)."""
-    buf = (ctypes.c_longlong * 256)()
-    _check(lib().shuf_debug_clocks(plan.handle, _stream(stream), buf, 256), "shuf_debug_clocks", plan)
-    return [int(buf[i]) for i in range(256)]
+    buf = (ctypes.c_longlong * 512)()
+    _check(lib().shuf_debug_clocks(plan.handle, _stream(stream), buf, 512), "shuf_debug_clocks", plan)
+    return [int(buf[i]) for i in range(512)]
 
 
 def shuf_destroy(plan: Plan):

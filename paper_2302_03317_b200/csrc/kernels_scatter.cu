@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
     const bool dbgc = blockIdx.x == 0 && tid == 0 && lp.level == 0;
     for (uint32_t it = 0; cur.chunk < nchunk; ++it) {
         const bool dbg = dbgc && it < 40;
-        if (dbg) rp.hdr->clk[it * 6 + 0] = clock64();
+        if (dbg) rp.hdr->sclk[it * 6 + 0] = clock64();
         // ---- next tile of this CTA's sequence -> the other buffer (free since
         //      the previous iteration's copy-out)
         STile nxt = cur;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
                 }
             }
         }
-        if (dbg) rp.hdr->clk[it * 6 + 1] = clock64();
+        if (dbg) rp.hdr->sclk[it * 6 + 1] = clock64();
         // ---- wait for this tile's data, publish the counts
         if (it & 1u) {
             mbar_wait(&bar[1], ph1);
@@ -261,13 +261,13 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
             ph0 ^= 1u;
         }
         __syncthreads();
-        if (dbg) rp.hdr->clk[it * 6 + 2] = clock64();
+        if (dbg) rp.hdr->sclk[it * 6 + 2] = clock64();
         // ---- 2. scan: (bucket, warp)-major exclusive prefix of the counts ->
         //      per-warp slot bases; bst = bucket starts of the tile
         if (NARROW) scan_counters32<kSW * 32>(tab, kSW, k, bst, wsum);
         else scan_counters<kSW * 32>(tab, kSW, k, bst, wsum);
         __syncthreads();
-        if (dbg) rp.hdr->clk[it * 6 + 3] = clock64();
+        if (dbg) rp.hdr->sclk[it * 6 + 3] = clock64();
         // ---- 3. place: values to registers, then each to its slot in buf
         {
             E* el = reinterpret_cast<E*>(buf + ((cur.q0 * EB) & 15u));
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
             running[b] += bst[b + 1] - bst[b];
         }
         __syncthreads();
-        if (dbg) rp.hdr->clk[it * 6 + 4] = clock64();
+        if (dbg) rp.hdr->sclk[it * 6 + 4] = clock64();
         // ---- 4. copy-out: slot s -> dst[delta[bucket(s)] + s]; consecutive
         //      lanes take consecutive slots, so each warp store covers the
         //      1-3 runs that meet its 32 slots (coalesced)
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
             for (uint32_t x = tid; x < cnt; x += kSW * 32) dst[delta[slotb[x]] + x] = el[x];
         }
         __syncthreads();
-        if (dbg) rp.hdr->clk[it * 6 + 5] = clock64();
+        if (dbg) rp.hdr->sclk[it * 6 + 5] = clock64();
         new_chunk = next_chunk;
         cur = nxt;
         cnt = ncnt;

@@ -326,6 +326,10 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     rp.rank_ordered = (uint32_t)p->rank_ordered;
     rp.fin_nbuf = p->fin_nbuf;
     rp.fast = (uint32_t)p->fast;
+    {
+        const char* dbg = std::getenv("SHUF_DBG");
+        rp.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
+    }
     rp.flags = sc + p->lay.flags;
     uint64_t launches = 0;
     if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
@@ -479,7 +483,7 @@ extern "C" shuf_status shuf_debug_clocks(shuf_plan_t p, void* stream, long long*
     if (!p->last_hdr) return SHUF_OK;
     cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
     if (e) return cuda_fail(p, e);
-    if (count > 256) count = 256;
+    if (count > 512) count = 512;  // [0, 256): fast finish, [256, 512): level-0 scatter
     if ((e = cudaMemcpy(out, p->last_hdr->clk, count * sizeof(long long), cudaMemcpyDeviceToHost))) return cuda_fail(p, e);
     return SHUF_OK;
 }

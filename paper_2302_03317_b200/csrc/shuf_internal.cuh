@@ -58,6 +58,7 @@ struct Header {
     uint64_t finished;                    // elements written by the fused finish
     uint64_t fy_elems;                    // elements in Fisher-Yates leaves
     long long clk[256];                   // phase timestamps of CTA 0 of the fast finish (shuf_debug_clocks)
+    long long sclk[256];                  // phase timestamps of CTA 0 of the level-0 HBM scatter
 };
 
 // Byte offsets of every region inside the caller's scratch buffer.
@@ -94,6 +95,7 @@ struct RunParams {
     uint32_t fin_nbuf;      // finish-kernel data buffers (2 = items double-buffered)
     uint32_t fast;          // 1: k_finish_fast runs first; the general finish takes flagged children only
     unsigned char* flags;   // per-child flags of the current level (ScratchLayout::flags)
+    uint32_t dbg;           // timing experiments only (SHUF_DBG): skip parts of the fast finish
 };
 
 struct LevelParams {

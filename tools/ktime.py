@@ -30,23 +30,23 @@ print(f"{wl}: {e0.elapsed_time(e1) / reps:.3f} ms/shuffle (stream-ordered, no pe
 prof = shuf.shuf_profile_run(plan, x, scratch, None)
 for k, (ms, n) in prof.items():
     print(f"  {k:8s} {ms:8.3f} ms  launches={n}")
-print("device error", shuf.shuf_last_device_error(plan))
+print("device error", shuf.shuf_last_device_error(plan), "env SHUF_FAST_FINISH =", os.environ.get("SHUF_FAST_FINISH"))
 shuf.shuf_run(plan, x, scratch)
 c = shuf.shuf_debug_clocks(plan)
 if "--scatter" in sys.argv:
     print("scatter CTA 0 level 0 tile phases (cycles): draws+count, wait+sync, scan, place, copyout, total")
     for it in range(1, 30):
-        t = c[it * 6: it * 6 + 6]
+        t = c[256 + it * 6: 256 + it * 6 + 6]
         if t[0] == 0:
             break
-        nx = c[(it + 1) * 6]
+        nx = c[256 + (it + 1) * 6]
         print(f"  tile {it}: {t[1]-t[0]:6d} {t[2]-t[1]:6d} {t[3]-t[2]:6d} {t[4]-t[3]:6d} {t[5]-t[4]:6d}  total {nx - t[0] if nx else 0:6d}")
     sys.exit(0)
-print("fast-finish CTA 0 phase clocks per item (cycles from the start of phase A)")
+print("fast-finish CTA 0 per item (cycles): scan+wait, place, partners, FY, FY||draws+count(next), store+rotate, total")
 for it in range(1, 12):
-    a0, fy, dc, sc, pl, pa = c[it * 6: it * 6 + 6]
-    if a0 == 0:
+    t = c[it * 6: it * 6 + 6]
+    if t[0] == 0:
         break
     nxt = c[(it + 1) * 6]
-    print(f"  item {it}: draw+count {dc - a0:6d}  fy_end {fy - a0:6d}  scan_end {sc - a0:6d}"
-          f"  place_end {pl - a0:6d}  partners_end {pa - a0:6d}  total {nxt - a0 if nxt else 0:6d}")
+    print(f"  item {it}: {t[1]-t[0]:6d} {t[2]-t[1]:6d} {t[3]-t[2]:6d} {t[4]-t[3]:6d} {t[5]-t[4]:6d} "
+          f"{nxt - t[5] if nxt else 0:6d}  total {nxt - t[0] if nxt else 0:6d}")

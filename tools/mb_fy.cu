@@ -23,13 +23,16 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 //         final values to a contiguous out buffer, pipelined depth 1.
 // MODE 1: contiguous leaf, in-place swaps, pipelined depth 1.
 // MODE 2: column layout, in place, plain (no pipelining).
-// MODE 3: column layout, in place, partners as u16 byte offsets, unrolled x4.
+// MODE 3: column layout, in place, unrolled x4 (partner words per thread contiguous).
+// MODE 4: column layout, in place, unrolled x4, partner words interleaved (conflict-free).
+// MODE 5: contiguous leaf, in place, unrolled x4, partner words interleaved.
+// MODE 6: column layout, pull to a contiguous out buffer, unrolled x4, interleaved partners.
 template <int MODE, int NT>
 __global__ void __launch_bounds__(NT, 1) k_fy(uint32_t* sink) {
     extern __shared__ uint32_t sm[];
-    constexpr int NB = MODE == 0 ? 2 : 1;        // word buffers of NT*M
+    constexpr int NB = (MODE == 0 || MODE == 6) ? 2 : 1;  // word buffers of NT*M
     uint32_t* col = sm;                          // NT*M words
-    uint32_t* out = MODE == 0 ? sm + NT * M : sm;
+    uint32_t* out = (MODE == 0 || MODE == 6) ? sm + NT * M : sm;
     unsigned char* jb = (unsigned char*)(sm + NB * NT * M);  // NT*M bytes
     const uint32_t t = threadIdx.x;
     for (uint32_t i = t; i < NT * M; i += NT) {
@@ -90,6 +93,28 @@ __global__ void __launch_bounds__(NT, 1) k_fy(uint32_t* sink) {
                 c[i * NT] = y;
             }
             acc += c[(rep & 63) * NT];
+        } else if (MODE == 4 || MODE == 5 || MODE == 6) {
+            const uint32_t* jwi = (const uint32_t*)jb;  // word w of thread t at jwi[w*NT + t]
+            uint32_t* c = MODE == 5 ? out + t * M : col + t;
+            constexpr int S = MODE == 5 ? 1 : NT;
+            uint32_t* o = out + t * M;
+            uint32_t* ci = c + (M - 1) * S;
+            for (int w = (M / 4) - 1; w >= 0; --w) {
+                const uint32_t pk = jwi[w * NT + t];
+#pragma unroll
+                for (int q = 3; q >= 0; --q) {
+                    if (w == 0 && q == 0) break;
+                    const uint32_t j = (pk >> (q * 8)) & 0xFF;
+                    uint32_t* cj = c + j * S;
+                    const uint32_t x = *ci, y = *cj;
+                    *cj = x;
+                    if (MODE == 6) o[w * 4 + q] = y;
+                    else *ci = y;
+                    ci -= S;
+                }
+            }
+            if (MODE == 6) o[0] = c[0];
+            acc += MODE == 6 ? o[rep & 63] : c[(rep & 63) * S];
         } else {
             // partners unpacked 4 at a time, explicit unroll, pointer walking
             uint32_t* c = col + t;
@@ -115,7 +140,7 @@ __global__ void __launch_bounds__(NT, 1) k_fy(uint32_t* sink) {
 
 template <int MODE, int NT>
 static void run(const char* name, int sms, int clk_khz, uint32_t* d) {
-    const int smem = NT * M * 4 * (MODE == 0 ? 2 : 1) + NT * M;
+    const int smem = NT * M * 4 * ((MODE == 0 || MODE == 6) ? 2 : 1) + NT * M;
     cudaFuncSetAttribute(k_fy<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_fy<MODE, NT><<<sms, NT, smem>>>(d);
     cudaDeviceSynchronize();
@@ -140,14 +165,12 @@ int main() {
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     uint32_t* d;
     cudaMalloc(&d, 64);
-    run<0, 256>("column pull pipelined", sms, clk, d);
-    run<1, 256>("contiguous in-place pipelined", sms, clk, d);
-    run<2, 256>("column in-place plain", sms, clk, d);
     run<3, 256>("column in-place unrolled", sms, clk, d);
-    run<1, 512>("contiguous in-place pipelined", sms, clk, d);
-    run<2, 512>("column in-place plain", sms, clk, d);
-    run<3, 512>("column in-place unrolled", sms, clk, d);
-    run<2, 768>("column in-place plain", sms, clk, d);
-    run<3, 768>("column in-place unrolled", sms, clk, d);
+    run<4, 256>("column in-place unr, jw interleaved", sms, clk, d);
+    run<5, 256>("contig in-place unr, jw interleaved", sms, clk, d);
+    run<6, 256>("column pull unr, jw interleaved", sms, clk, d);
+    run<4, 512>("column in-place unr, jw interleaved", sms, clk, d);
+    run<5, 512>("contig in-place unr, jw interleaved", sms, clk, d);
+    run<5, 1024>("contig in-place unr, jw interleaved", sms, clk, d);
     return 0;
 }
