@@ -108,7 +108,8 @@ enum {
     SHUF_K_PLAN = 3,    /* next-level segment planner                        */
     SHUF_K_SCATTER = 4, /* HBM stable scatter                                */
     SHUF_K_FINISH = 5,  /* fused shared-memory finish (levels + FY leaves)   */
-    SHUF_K_CLASSES = 6
+    SHUF_K_LEAF = 6,    /* leaf kernel: FY of HBM-level leaves / short segments */
+    SHUF_K_CLASSES = 7
 };
 
 /* Measurement hook: enqueue the same work as shuf_run (d_offsets == NULL) or
@@ -122,8 +123,9 @@ shuf_status shuf_profile_run(shuf_plan_t p, void *ptr, const uint64_t *d_offsets
 /* Measurement counters of the last run on this plan (synchronises):
  * out[0] = elements written by the fused finish, out[1] = elements in
  * Fisher-Yates leaves, out[2+2l] = elements scattered through HBM at level l,
- * out[3+2l] = elements scattered in shared memory at level l (l < 256).
- * Writes min(count, 514) entries; the rest are zero. */
+ * out[3+2l] = elements scattered in shared memory at level l (l < 256),
+ * out[514] = elements written by the leaf kernel.
+ * Writes min(count, 515) entries; the rest are zero. */
 shuf_status shuf_last_run_stats(shuf_plan_t p, void *stream, uint64_t *out, uint32_t count);
 
 /* Debug: phase timestamps (clock64) recorded by CTA 0 of the fast finish

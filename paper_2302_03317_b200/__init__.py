@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = [
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
     "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks",
 ]
-KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish"]
+KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish", "leaf"]
 
 
 class ShufError(RuntimeError):
@@ -209,25 +209,26 @@ def shuf_profile_run(plan: Plan, x, scratch, d_offsets=None, stream=None):
     """Same work as shuf_run / shuf_segmented with every launch bracketed by CUDA
     events on the stream; synchronises.  Returns {class: (ms, launches)}."""
     _check_data(plan, x)
-    ms = (ctypes.c_float * 6)()
-    cnt = (ctypes.c_uint32 * 6)()
+    ms = (ctypes.c_float * len(KERNEL_CLASSES))()
+    cnt = (ctypes.c_uint32 * len(KERNEL_CLASSES))()
     offp = _dev_ptr(d_offsets, "offsets") if d_offsets is not None else None
     nseg = d_offsets.numel() - 1 if d_offsets is not None else 0
     _check(lib().shuf_profile_run(plan.handle, _dev_ptr(x, "x"), offp, nseg, _dev_ptr(scratch, "scratch"),
                                   scratch.numel() * scratch.element_size(), _stream(stream), ms, cnt),
            "shuf_profile_run", plan)
-    return {KERNEL_CLASSES[i]: (float(ms[i]), int(cnt[i])) for i in range(6)}
+    return {KERNEL_CLASSES[i]: (float(ms[i]), int(cnt[i])) for i in range(len(KERNEL_CLASSES))}
 
 
 def shuf_last_run_stats(plan: Plan, stream=None) -> dict:
     """Device counters of the last run (synchronises): per-level elements
     scattered in HBM / shared memory, elements finished, elements in FY leaves."""
-    buf = (ctypes.c_uint64 * 514)()
-    _check(lib().shuf_last_run_stats(plan.handle, _stream(stream), buf, 514), "shuf_last_run_stats", plan)
+    buf = (ctypes.c_uint64 * 515)()
+    _check(lib().shuf_last_run_stats(plan.handle, _stream(stream), buf, 515), "shuf_last_run_stats", plan)
     hbm = [int(buf[2 + 2 * l]) for l in range(256)]
     sm = [int(buf[3 + 2 * l]) for l in range(256)]
     top = max([l + 1 for l in range(256) if hbm[l] or sm[l]] or [0])
-    return {"finished": int(buf[0]), "fy_elems": int(buf[1]), "scattered_hbm": hbm[:top], "scattered_smem": sm[:top]}
+    return {"finished": int(buf[0]), "fy_elems": int(buf[1]), "leafed": int(buf[514]),
+            "scattered_hbm": hbm[:top], "scattered_smem": sm[:top]}
 
 
 def shuf_debug_clocks(plan: Plan, stream=None) -> list:

@@ -190,4 +190,53 @@ __device__ __forceinline__ void scan_counters32(uint32_t* C, uint32_t nw, uint32
     __syncthreads();
 }
 
+// ---------------------------------------------------- Fisher-Yates ------
+// One Fisher-Yates step (Fig. 1): swap(A[i], A[j]), j = fy(q, i) from the
+// 16-bit lane v of the step's Philox group (D5, Lemire16).
+template <typename E>
+__device__ __forceinline__ void fy_step(E* A, uint32_t i, uint32_t v, PhiloxKey key, uint64_t q) {
+    const uint32_t s = i + 1, mm = v * s;
+    uint32_t j = mm >> 16;
+    if (__builtin_expect((mm & 0xFFFFu) < s, 0)) j = fy16_from_lane(v, key, q, i);  // exact rejection test
+    const E t = A[i];
+    A[i] = A[j];
+    A[j] = t;
+}
+
+// Fisher-Yates (Fig. 1) of the leaf A[0 .. cm) whose first
+// element is problem position q: for i = cm-1 .. 1, swap(i, fy(q, i)) with
+// the partner drawn for (leaf id q, step i) (D5): one Philox call per 8
+// steps, so every lane of a warp (each on its own leaf) draws in lockstep.
+// The partial top group is peeled so the full groups run without checks.
+template <int EB>
+__device__ __forceinline__ void fy_leaf(unsigned char* el, uint32_t c, uint32_t cm, uint64_t q, PhiloxKey key) {
+    using E = typename ElemT<EB>::type;
+    if (cm < 2) return;
+    E* A = reinterpret_cast<E*>(el) + c;
+    const uint32_t gt = (cm - 1) >> 3;
+    {  // top group: steps cm-1 .. max(8*gt, 1)
+        const uint4 w = fy16_group_words(key, q, gt);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int32_t jj = 7; jj >= 0; --jj) {
+            const uint32_t i = gt * 8u + (uint32_t)jj;
+            if (i < cm && i >= 1) fy_step(A, i, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+        }
+    }
+    for (int32_t g = (int32_t)gt - 1; g >= 1; --g) {  // full groups
+        const uint4 w = fy16_group_words(key, q, (uint32_t)g);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+        E* Ag = A;
+#pragma unroll
+        for (int32_t jj = 7; jj >= 0; --jj)
+            fy_step(Ag, (uint32_t)g * 8u + (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+    }
+    if (gt >= 1) {  // group 0: steps 7 .. 1
+        const uint4 w = fy16_group_words(key, q, 0u);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int32_t jj = 7; jj >= 1; --jj) fy_step(A, (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+    }
+}
+
 }  // namespace shuf

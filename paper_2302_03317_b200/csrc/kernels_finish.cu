@@ -51,6 +51,7 @@ struct FinCtl {
     uint32_t b, bend;    // iterator: child cursor within the unit
     uint64_t seg_start, seg_origin, seg_key;
     uint64_t ub[kUnit + 1];  // unit child boundaries (relative to seg_start)
+    uint64_t rec;            // item record index (defer mode)
     unsigned long long st_finished, st_smem[32];
 };
 
@@ -157,55 +158,6 @@ __device__ __forceinline__ void item_store(const Item& it, unsigned char* dst, c
     else if (tid >= 64 && tid - 64 < nt)
         *reinterpret_cast<uint32_t*>(dst + tBeg + 4 * (tid - 64)) =
             *reinterpret_cast<const uint32_t*>(buf + (tBeg - fl) + 4 * (tid - 64));
-}
-
-// ---------------------------------------------------- Fisher-Yates ------
-// One Fisher-Yates step (Fig. 1): swap(A[i], A[j]), j = fy(q, i) from the
-// 16-bit lane v of the step's Philox group (D5, Lemire16).
-template <typename E>
-__device__ __forceinline__ void fy_step(E* A, uint32_t i, uint32_t v, PhiloxKey key, uint64_t q) {
-    const uint32_t s = i + 1, mm = v * s;
-    uint32_t j = mm >> 16;
-    if (__builtin_expect((mm & 0xFFFFu) < s, 0)) j = fy16_from_lane(v, key, q, i);  // exact rejection test
-    const E t = A[i];
-    A[i] = A[j];
-    A[j] = t;
-}
-
-// Fisher-Yates (Fig. 1) of the leaf A[0 .. cm) whose first
-// element is problem position q: for i = cm-1 .. 1, swap(i, fy(q, i)) with
-// the partner drawn for (leaf id q, step i) (D5): one Philox call per 8
-// steps, so every lane of a warp (each on its own leaf) draws in lockstep.
-// The partial top group is peeled so the full groups run without checks.
-template <int EB>
-__device__ __forceinline__ void fy_leaf(unsigned char* el, uint32_t c, uint32_t cm, uint64_t q, PhiloxKey key) {
-    using E = typename ElemT<EB>::type;
-    if (cm < 2) return;
-    E* A = reinterpret_cast<E*>(el) + c;
-    const uint32_t gt = (cm - 1) >> 3;
-    {  // top group: steps cm-1 .. max(8*gt, 1)
-        const uint4 w = fy16_group_words(key, q, gt);
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int32_t jj = 7; jj >= 0; --jj) {
-            const uint32_t i = gt * 8u + (uint32_t)jj;
-            if (i < cm && i >= 1) fy_step(A, i, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
-        }
-    }
-    for (int32_t g = (int32_t)gt - 1; g >= 1; --g) {  // full groups
-        const uint4 w = fy16_group_words(key, q, (uint32_t)g);
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-        E* Ag = A;
-#pragma unroll
-        for (int32_t jj = 7; jj >= 0; --jj)
-            fy_step(Ag, (uint32_t)g * 8u + (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
-    }
-    if (gt >= 1) {  // group 0: steps 7 .. 1
-        const uint4 w = fy16_group_words(key, q, 0u);
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int32_t jj = 7; jj >= 1; --jj) fy_step(A, (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
-    }
 }
 
 // ---------------------------------------------------- one smem level ----
@@ -343,11 +295,26 @@ __device__ __forceinline__ void process_item(const RunParams& rp, const Fin& F, 
         // OUT was last read by the previous item's bulk store
         if (tid == 0) bulk_wait_read0();
         smem_level<EB, NARROW, ORD>(rp, F, in, out, 0, m, P0, it.level, key, true);
-        const bool deep = any_big_child(rp, F) && it.level + 1 < rp.max_levels;
+        const bool big = any_big_child(rp, F);
+        const bool deep = big && it.level + 1 < rp.max_levels;
         if (!deep && next) item_load<EB>(*next, src, F.in(), F.bar());  // IN is free: overlap the next load
-        if (tid == 0) ctl->nfront = 0;
+        if (tid == 0) {
+            ctl->nfront = 0;
+            if (rp.defer && !big) ctl->rec = atomicAdd((unsigned long long*)&rp.hdr->nitems, 1ull);
+        }
         __syncthreads();
-        handle_children<EB>(rp, F, out, 0, m, P0, it.level, key, F.front(0), fy_local);
+        if (rp.defer && !big) {
+            // every child is a leaf: record the item; the leaf kernel runs Fisher-Yates on them
+            unsigned char* r = rp.items + ctl->rec * item_rec_stride(rp.k);
+            if (tid == 0) {
+                reinterpret_cast<uint64_t*>(r)[0] = it.start;
+                reinterpret_cast<uint64_t*>(r)[1] = it.origin;
+                reinterpret_cast<uint64_t*>(r)[2] = it.key;
+            }
+            for (uint32_t b = tid; b <= rp.k; b += NTF) reinterpret_cast<uint16_t*>(r + 24)[b] = (uint16_t)F.bst()[b];
+        } else {
+            handle_children<EB>(rp, F, out, 0, m, P0, it.level, key, F.front(0), fy_local);
+        }
         __syncthreads();
         uint32_t nf = ctl->nfront, cur = 0, lv = it.level + 1;
         __syncthreads();
@@ -469,6 +436,7 @@ struct ChildIter {
             for (uint32_t b = ctl->b; b < ctl->bend; ++b) {
                 const uint64_t s0 = ctl->ub[b - b0], len = ctl->ub[b - b0 + 1] - s0;
                 if (len == 0 || len > rp->S_fuse) continue;
+                if (rp->leafk && len <= rp->L) continue;  // the leaf kernel's
                 if (lp->dst == rp->buf0 && !item_permutes(*rp, (uint32_t)len, lvl)) continue;
                 // children finished by k_finish_fast carry flag 0
                 if (rp->fast && rp->flags[(ctl->u / groups) * rp->k + b] == 0) continue;
@@ -531,6 +499,7 @@ struct SegIter {
                 ctl->u += gridDim.x;
                 const uint64_t a = off[si], b = off[si + 1];
                 if (b <= a || b - a > rp->S_fuse) continue;
+                if (rp->leafk && b - a <= rp->L) continue;  // the leaf kernel's
                 if (!item_permutes(*rp, (uint32_t)(b - a), 0u)) continue;
                 Item& it = ctl->items[slot];
                 it.start = a;

@@ -1,0 +1,273 @@
+// Leaf kernel: Fisher-Yates (Fig. 1) of every
+// leaf -- a segment of at most L elements -- with one thread per leaf and
+// many leaves in flight per SM.
+//
+// Leaves come in units of up to 32 consecutive children of one segment of a
+// level (children b = 32g .. 32g+31; a level's children of at most L
+// elements are leaves, D6), or of up to 32 consecutive user segments at
+// level 0 (D7).  A warp takes a unit and processes its leaves in batches
+// that fit the warp's shared-memory slot: lane x owns leaf x of the batch,
+// loads it with one bulk async copy (TMA engine; <= 3 unaligned words at
+// each end by 4-byte asynchronous copies), runs Fisher-Yates on it with the
+// D5 draws of (leaf id = problem position of the leaf start, step), and
+// stores it back to ptr the same way.  No CTA barriers: warps are
+// independent, so the leaf chains of up to 32 x (warps per SM) leaves hide
+// each other's latency.
+#include <cuda_runtime.h>
+
+#include "block_ops.cuh"
+#include "shuf_internal.cuh"
+
+namespace shuf {
+
+extern __shared__ __align__(16) unsigned char lsm[];
+
+constexpr uint32_t kLeafThreads = 128;  // 4 warps per CTA
+constexpr uint32_t kLeafWarps = kLeafThreads / 32;
+
+// Slot bytes per warp: at least 16 KiB, and room for one leaf of L elements.
+__host__ __device__ inline uint32_t leaf_slot_bytes(uint32_t eb, uint32_t L) {
+    uint32_t s = (L * eb + 32 + 15) & ~15u;
+    return s < 16384u ? 16384u : s;
+}
+uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L) { return kLeafWarps * (leaf_slot_bytes(eb, L) + 16); }
+
+struct Leaf {
+    uint64_t start, len, origin, key;
+};
+
+// Leaf `lane` of unit u of a level's children: children 32g .. 32g+31 of
+// segment s, u = s * ceil(k/32) + g.
+struct ChildLeaves {
+    const LevelParams* lp;
+    uint32_t k, groups;
+    __device__ __forceinline__ uint64_t units() const { return (uint64_t)lp->ctr->nseg * groups; }
+    __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
+        Leaf f{0, 0, 0, 0};
+        const uint32_t s = (uint32_t)(u / groups), b = (uint32_t)(u % groups) * 32u + lane;
+        if (b < k) {
+            const SegDesc sg = lp->segs[s];
+            const uint64_t base0 = lp->prefix[sg.cbase];
+            const uint64_t s0 = lp->prefix[sg.cbase + (uint64_t)b * sg.nchunks] - base0;
+            const uint64_t s1 = (b + 1 < k) ? lp->prefix[sg.cbase + (uint64_t)(b + 1) * sg.nchunks] - base0 : sg.len;
+            f.start = sg.start + s0;
+            f.len = s1 - s0;
+            f.origin = sg.origin;
+            f.key = sg.key;
+        }
+        return f;
+    }
+};
+
+// User segments 32u .. 32u+31 (segmented mode at level 0, or the root).
+struct SegLeaves {
+    const uint64_t* off;
+    uint64_t nsegs, seed;
+    __device__ __forceinline__ uint64_t units() const { return (nsegs + 31) / 32; }
+    __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
+        Leaf f{0, 0, 0, 0};
+        const uint64_t s = u * 32u + lane;
+        if (s < nsegs) {
+            f.start = off[s];
+            const uint64_t e = off[s + 1];
+            f.len = e > f.start ? e - f.start : 0;
+            f.origin = f.start;
+            f.key = seed + s * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
+        }
+        return f;
+    }
+};
+
+// Leaf `lane` of unit u of the recorded fused items: children 32g .. 32g+31
+// of item r, u = r * ceil(k/32) + g (records: shuf_internal.cuh).
+struct ItemLeaves {
+    const unsigned char* items;
+    const uint64_t* nitems;
+    uint32_t k, groups, stride;
+    __device__ __forceinline__ uint64_t units() const { return *nitems * groups; }
+    __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
+        Leaf f{0, 0, 0, 0};
+        const uint64_t r = u / groups;
+        const uint32_t b = (uint32_t)(u % groups) * 32u + lane;
+        if (b < k) {
+            const unsigned char* rec = items + r * stride;
+            const uint16_t* o = reinterpret_cast<const uint16_t*>(rec + 24);
+            const uint32_t s0 = o[b], s1 = o[b + 1];
+            f.start = reinterpret_cast<const uint64_t*>(rec)[0] + s0;
+            f.len = s1 - s0;
+            f.origin = reinterpret_cast<const uint64_t*>(rec)[1];
+            f.key = reinterpret_cast<const uint64_t*>(rec)[2];
+        }
+        return f;
+    }
+};
+
+template <int EB, class Src>
+__device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned char* src, const Src& ls,
+                                           uint32_t slot_bytes) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    unsigned char* slot = lsm + warp * (slot_bytes + 16);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(slot + slot_bytes);
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    const uint64_t units = ls.units();
+    const bool copy_out = src != rp.buf0;
+    unsigned long long fyn = 0, fin = 0;
+    for (uint64_t u = (uint64_t)blockIdx.x * kLeafWarps + warp; u < units; u += (uint64_t)gridDim.x * kLeafWarps) {
+        const Leaf lf = ls.get(u, lane);
+        const uint64_t start = lf.start, len = lf.len, origin = lf.origin, key = lf.key;
+        const bool fy = len >= 2 && len <= rp.L && rp.run_leaves;
+        const bool mine = len >= 1 && len <= rp.L && (fy || copy_out);
+        if (mine) fin += len;
+        // ---- batches: leaves in lane order, packed into the slot
+        uint32_t todo = __ballot_sync(0xFFFFFFFFu, mine);
+        const uint32_t need = mine ? (((uint32_t)len * EB + 32 + 15) & ~15u) : 0u;
+        while (todo) {
+            // the batch: the longest run of pending lanes (in lane order) that fits
+            const uint32_t first = __ffs(todo) - 1;
+            uint32_t off = 0;  // my slot offset if I am in the batch
+            bool inb = false;
+            {
+                const uint32_t pend = (todo >> lane) & 1u;
+                const uint32_t v = pend && lane >= first ? need : 0u;
+                const uint32_t incl = warp_inclusive_sum(v);
+                inb = pend && lane >= first && incl <= slot_bytes;
+                off = incl - v;
+            }
+            const uint32_t batch = __ballot_sync(0xFFFFFFFFu, inb);
+            todo &= ~batch;
+            // ---- load: aligned body by one bulk copy per leaf, ends by 4-byte copies
+            uint64_t x0 = 0, x1 = 0, A = 0, B = 0;
+            uint32_t body = 0;
+            if (inb) {
+                x0 = start * EB;
+                x1 = (start + len) * EB;
+                A = (x0 + 15) & ~15ull;
+                B = x1 & ~15ull;
+                body = B > A ? (uint32_t)(B - A) : 0u;
+            }
+            uint32_t tot = body;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+            unsigned char* lb = slot + off;  // leaf buffer: element e at lb + (x0 & 15) + e*EB
+            if (lane == 0) mbar_arrive_expect_tx(bar, tot);
+            __syncwarp();
+            if (inb) {
+                if (body) {
+                    fence_proxy_async();
+                    bulk_g2s(lb + (A - (x0 & ~15ull)), src + A, body, bar);
+                }
+                const uint64_t hEnd = body ? A : x1, tBeg = body ? B : x1;
+                for (uint64_t x = x0; x < hEnd; x += 4)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(lb + (x - (x0 & ~15ull)))),
+                                 "l"(src + x)
+                                 : "memory");
+                for (uint64_t x = tBeg; x < x1; x += 4)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(lb + (x - (x0 & ~15ull)))),
+                                 "l"(src + x)
+                                 : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            // ---- Fisher-Yates of my leaf (D5 draws keyed by the leaf start)
+            if (inb && fy) {
+                fy_leaf<EB>(lb + (x0 & 15u), 0u, (uint32_t)len, start - origin, make_key(key));
+                fyn += len;
+            }
+            // ---- store: aligned body by one bulk copy, ends by words
+            if (inb) {
+                if (body) {
+                    fence_proxy_async();
+                    bulk_s2g(rp.buf0 + A, lb + (A - (x0 & ~15ull)), body);
+                    bulk_commit();
+                }
+                const uint64_t hEnd = body ? A : x1, tBeg = body ? B : x1;
+                for (uint64_t x = x0; x < hEnd; x += 4)
+                    *reinterpret_cast<uint32_t*>(rp.buf0 + x) =
+                        *reinterpret_cast<const uint32_t*>(lb + (x - (x0 & ~15ull)));
+                for (uint64_t x = tBeg; x < x1; x += 4)
+                    *reinterpret_cast<uint32_t*>(rp.buf0 + x) =
+                        *reinterpret_cast<const uint32_t*>(lb + (x - (x0 & ~15ull)));
+                bulk_wait_read0();  // the slot is read out before the next batch reuses it
+            }
+            __syncwarp();
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        fyn += __shfl_xor_sync(0xFFFFFFFFu, fyn, o);
+        fin += __shfl_xor_sync(0xFFFFFFFFu, fin, o);
+    }
+    if (lane == 0) {
+        if (fyn) atomicAdd((unsigned long long*)&rp.hdr->fy_elems, fyn);
+        if (fin) atomicAdd((unsigned long long*)&rp.hdr->leafed, fin);
+    }
+    bulk_wait0();
+}
+
+template <int EB>
+__global__ void __launch_bounds__(kLeafThreads) k_leaf_children(RunParams rp, LevelParams lp) {
+    const ChildLeaves ls{&lp, rp.k, (rp.k + 31) / 32};
+    run_leaves<EB>(rp, lp.dst, ls, leaf_slot_bytes(EB, rp.L));
+}
+
+template <int EB>
+__global__ void __launch_bounds__(kLeafThreads) k_leaf_segments(RunParams rp, const uint64_t* __restrict__ off,
+                                                                 uint64_t nsegs) {
+    const SegLeaves ls{off, nsegs, rp.seed};
+    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
+}
+
+template <int EB>
+__global__ void __launch_bounds__(kLeafThreads) k_leaf_items(RunParams rp) {
+    const ItemLeaves ls{rp.items, &rp.hdr->nitems, rp.k, (rp.k + 31) / 32, item_rec_stride(rp.k)};
+    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
+}
+
+// mode: 0 children, 1 segments, 2 items
+static void* leaf_fn(uint32_t eb, int mode) {
+    switch (eb) {
+    case 4: return mode == 1 ? (void*)k_leaf_segments<4> : mode == 2 ? (void*)k_leaf_items<4> : (void*)k_leaf_children<4>;
+    case 8: return mode == 1 ? (void*)k_leaf_segments<8> : mode == 2 ? (void*)k_leaf_items<8> : (void*)k_leaf_children<8>;
+    default:
+        return mode == 1 ? (void*)k_leaf_segments<16> : mode == 2 ? (void*)k_leaf_items<16> : (void*)k_leaf_children<16>;
+    }
+}
+
+cudaError_t configure_leaf(uint32_t eb, uint32_t L) {
+    const uint32_t smem = leaf_smem_bytes(eb, L);
+    for (int mode = 0; mode < 3; ++mode) {
+        cudaError_t e = cudaFuncSetAttribute(leaf_fn(eb, mode), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, leaf_fn(eb, 0), kLeafThreads,
+                                                         leaf_smem_bytes(eb, L));
+}
+
+cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    void* args[] = {(void*)&rp, (void*)&lp};
+    return cudaLaunchKernel(leaf_fn(rp.eb, 0), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L),
+                            s);
+}
+
+cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
+                                 cudaStream_t s, int grid) {
+    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments};
+    return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L),
+                            s);
+}
+
+cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid) {
+    void* args[] = {(void*)&rp};
+    return cudaLaunchKernel(leaf_fn(rp.eb, 2), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L), s);
+}
+
+}  // namespace shuf

@@ -27,8 +27,8 @@ struct shuf_plan_s {
     // device setup (lazily, first run)
     bool dev_ready;
     int sms;
-    int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small, grid_fast;
-    int fast;
+    int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small, grid_fast, grid_leaf;
+    int fast, leafk, defer;
     int rank_ordered;
     uint32_t finish_smem, scatter_smem;
     int last_cuda_error;
@@ -108,6 +108,9 @@ static void compute_layout(shuf_plan_s* p) {
     }
     l.flags = off;
     off = align_up(off + l.max_segs * p->k, 256);
+    l.max_items = n / ((uint64_t)p->L + 1) + 1;
+    l.items = off;
+    off = align_up(off + l.max_items * item_rec_stride(p->k), 256);
     l.total = off;
 }
 
@@ -126,7 +129,12 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
         return nullptr;
     }
     uint32_t nbuf = 1;
-    const uint32_t S = pick_s_fuse(elem_bytes, k, L, &nbuf);
+    uint32_t S = pick_s_fuse(elem_bytes, k, L, &nbuf);
+    {  // SHUF_SFUSE=<elements>: a smaller fusable size (e.g. L: every level in HBM)
+        const char* sf = std::getenv("SHUF_SFUSE");
+        const long v = sf ? std::atol(sf) : 0;
+        if (v >= (long)L && v < (long)S) S = (uint32_t)v;
+    }
     if (L > S) {
         g_last_status = SHUF_ERR_UNSUPPORTED;
         return nullptr;
@@ -225,10 +233,22 @@ static cudaError_t device_setup(shuf_plan_s* p) {
                       : 0;
         if (p->fast && (e = configure_fast(p->eb, p->k))) return e;
     }
+    // leaf kernel (kernels_leaf.cu): SHUF_LEAF=0 keeps leaves in the finish kernel
+    {
+        const char* lf = std::getenv("SHUF_LEAF");
+        p->leafk = (lf && lf[0] == '0') ? 0 : 1;
+        if (p->leafk && leaf_smem_bytes(p->eb, p->L) > kSmemLimit) p->leafk = 0;
+        if (p->leafk && (e = configure_leaf(p->eb, p->L))) return e;
+        // SHUF_DEFER=1: fused items whose children are all leaves leave them to the leaf kernel
+        // (one more HBM round trip; measured slower on HOT)
+        const char* df = std::getenv("SHUF_DEFER");
+        p->defer = (p->leafk && df && df[0] == '1') ? 1 : 0;
+    }
     // persistent grids: SM count x resident CTAs per SM
-    int oh = 1, os = 1, osc = 1, of = 1;
+    int oh = 1, os = 1, osc = 1, of = 1, ol = 1;
     if ((e = occupancy_level(p->eb, p->k, &oh, &os, &osc))) return e;
     if ((e = occupancy_finish(p->eb, p->finish_smem, &of))) return e;
+    if (p->leafk && (e = occupancy_leaf(p->eb, p->L, &ol))) return e;
     auto clamp1 = [](int v) { return v < 1 ? 1 : v; };
     p->grid_hist = p->sms * clamp1(oh);
     p->grid_scan = p->sms * clamp1(os);
@@ -236,6 +256,7 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     p->grid_finish = p->sms * clamp1(of);
     p->grid_small = p->sms * 4;
     p->grid_fast = p->sms;
+    p->grid_leaf = p->sms * clamp1(ol);
     p->dev_ready = true;
     return cudaSuccess;
 }
@@ -326,6 +347,9 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     rp.rank_ordered = (uint32_t)p->rank_ordered;
     rp.fin_nbuf = p->fin_nbuf;
     rp.fast = (uint32_t)p->fast;
+    rp.leafk = (uint32_t)p->leafk;
+    rp.defer = (uint32_t)p->defer;
+    rp.items = sc + p->lay.items;
     {
         const char* dbg = std::getenv("SHUF_DBG");
         rp.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
@@ -337,9 +361,13 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     if (d_offsets) {
         LAUNCH(SHUF_K_INIT, launch_init_segmented(rp, lp0, d_offsets, nsegs, st, p->grid_small));
         LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, d_offsets, nsegs, st, p->grid_finish));
+        if (p->leafk) LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, d_offsets, nsegs, st, p->grid_leaf));
     } else {
         LAUNCH(SHUF_K_INIT, launch_init(rp, lp0, st, p->grid_small));
-        if (p->n <= p->S_fuse) LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
+        if (p->n <= p->S_fuse) {
+            if (p->leafk && p->n <= p->L) LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, hdr->root_off, 1, st, 1));
+            else LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
+        }
     }
     const uint32_t G = p->levels < max_levels ? p->levels : max_levels;
     for (uint32_t lv = 0; lv < G; ++lv) {
@@ -350,8 +378,11 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
         if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast(rp, lp, st, p->grid_fast));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
+        if (p->leafk) LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->grid_leaf));
         if (lv + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
     }
+    // leaves of the recorded fused items (all levels; they sit in ptr)
+    if (p->defer && (d_offsets || p->n > p->L)) LAUNCH(SHUF_K_LEAF, launch_leaf_items(rp, st, p->grid_leaf));
     p->last_launches = launches;
     return SHUF_OK;
 }
@@ -459,6 +490,7 @@ extern "C" shuf_status shuf_last_run_stats(shuf_plan_t p, void* stream, uint64_t
         if (2 + 2 * l < count) out[2 + 2 * l] = h.scattered_hbm[l];
         if (3 + 2 * l < count) out[3 + 2 * l] = h.scattered_smem[l];
     }
+    if (count > 514) out[514] = h.leafed;
     return SHUF_OK;
 }
 

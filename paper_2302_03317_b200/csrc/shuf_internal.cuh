@@ -57,6 +57,8 @@ struct Header {
     uint64_t scattered_smem[kMaxLevels];  // elements scattered in shared memory at level l
     uint64_t finished;                    // elements written by the fused finish
     uint64_t fy_elems;                    // elements in Fisher-Yates leaves
+    uint64_t leafed;                      // elements written by the leaf kernel
+    uint64_t nitems;                      // fused items recorded for the leaf kernel (RunParams::items)
     long long clk[256];                   // phase timestamps of CTA 0 of the fast finish (shuf_debug_clocks)
     long long sclk[256];                  // phase timestamps of CTA 0 of the level-0 HBM scatter
 };
@@ -71,6 +73,8 @@ struct ScratchLayout {
     uint64_t prefix[2];  // u64 per (bucket, chunk)
     uint64_t status[2];  // u64 per scan tile
     uint64_t flags;      // u8 per child of a level: 1 = finished by the general finish kernel
+    uint64_t items;      // item records (item_rec_stride bytes each), max_items of them
+    uint64_t max_items;
     uint64_t total;
     uint64_t max_segs, max_chunks, max_entries, max_tiles;
 };
@@ -96,7 +100,14 @@ struct RunParams {
     uint32_t fast;          // 1: k_finish_fast runs first; the general finish takes flagged children only
     unsigned char* flags;   // per-child flags of the current level (ScratchLayout::flags)
     uint32_t dbg;           // timing experiments only (SHUF_DBG): skip parts of the fast finish
+    uint32_t leafk;         // 1: leaves of HBM levels / user segments go to the leaf kernel (kernels_leaf.cu)
+    uint32_t defer;         // 1: the finish leaves the leaves of single-level items to the leaf kernel
+    unsigned char* items;   // item records: {start, origin, key} + u16 bucket starts [0, k]
 };
+
+// Item record of a fused item whose children are all leaves (defer mode):
+// u64 start, origin, key, then k+1 u16 child starts relative to start.
+__host__ __device__ inline uint32_t item_rec_stride(uint32_t k) { return (24u + 2u * (k + 1u) + 15u) & ~15u; }
 
 struct LevelParams {
     uint32_t level;     // l
@@ -134,6 +145,13 @@ cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaS
 cudaError_t configure_fast(uint32_t eb, uint32_t k);
 uint32_t fast_smem_bytes(uint32_t eb, uint32_t k);
 uint32_t fast_max_elems(uint32_t eb);
+cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
+                                 cudaStream_t s, int grid);
+cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid);
+cudaError_t configure_leaf(uint32_t eb, uint32_t L);
+cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks);
+uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L);
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);

@@ -139,27 +139,36 @@ def test_documented_match_rank_path_bit_exact():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_fast_finish_path_bit_exact():
-    """The experimental warp-specialised finish kernel (SHUF_FAST_FINISH=1,
-    kernels_fast.cu) is chosen per process; it must give the same bits on the
-    shapes it takes (one shared-memory level + leaves) and hand everything
-    else to the general kernel."""
+_ENV_CASES = (
+    "import sys; sys.path.insert(0, %r)\n"
+    "import numpy as np, oracle\n"
+    "from tests.gpu_util import gpu_shuffle, gpu_segmented\n"
+    "cases = [(3_000_000, 256, 4096, 11), (1 << 20, 256, 4096, 1), (300_001, 1000, 50, 7), (5000, 16, 100, 4),\n"
+    "         (777_777, 7, 300, 6), (2_000_000, 64, 40, 3), (4000, 256, 4096, 2), (20_000, 256, 16, 3)]\n"
+    "for n, k, L, seed in cases:\n"
+    "    a = np.arange(n, dtype=np.uint32)\n"
+    "    assert (gpu_shuffle(a, k, L, seed) == oracle.shuffle(a, k, L, seed)).all(), (n, k, L, seed)\n"
+    "b = np.arange(400_000, dtype=np.uint64) * 3\n"
+    "assert (gpu_shuffle(b, 256, 4096, 5) == oracle.shuffle(b, 256, 4096, 5)).all()\n"
+    "off = np.array([0, 0, 1, 3000, 3000, 9000, 9001, 60000, 64000], dtype=np.uint64)\n"
+    "c = np.arange(int(off[-1]), dtype=np.uint32)\n"
+    "assert (gpu_segmented(c, off, 64, 4096, 5) == oracle.segmented(c, off, 64, 4096, 5)).all()\n"
+    "print('ok')\n")
+
+
+@pytest.mark.parametrize("env", [{"SHUF_FAST_FINISH": "1"}, {"SHUF_LEAF": "0"}, {"SHUF_DEFER": "1"},
+                                 {"SHUF_DEFER": "1", "SHUF_RANK_MODE": "match"}],
+                         ids=["fast_finish", "no_leaf_kernel", "deferred_leaves", "deferred_leaves_match"])
+def test_alternate_routes_bit_exact(env):
+    """Routes chosen per process by environment (kernels_fast.cu's warp-
+    specialised finish; leaves in the finish kernel instead of the leaf
+    kernel; leaves of fused items deferred to the leaf kernel) must give the
+    same bits as the oracle on every shape, handing whatever they do not take
+    to the general kernels."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = (
-        "import sys; sys.path.insert(0, %r)\n"
-        "import numpy as np, oracle\n"
-        "from tests.gpu_util import gpu_shuffle\n"
-        "cases = [(3_000_000, 256, 4096, 11), (1 << 20, 256, 4096, 1), (300_001, 1000, 50, 7), (5000, 16, 100, 4),\n"
-        "         (777_777, 7, 300, 6), (2_000_000, 64, 40, 3)]\n"
-        "for n, k, L, seed in cases:\n"
-        "    a = np.arange(n, dtype=np.uint32)\n"
-        "    assert (gpu_shuffle(a, k, L, seed) == oracle.shuffle(a, k, L, seed)).all(), (n, k, L, seed)\n"
-        "b = np.arange(400_000, dtype=np.uint64) * 3\n"
-        "assert (gpu_shuffle(b, 256, 4096, 5) == oracle.shuffle(b, 256, 4096, 5)).all()\n"
-        "print('ok')\n" % root)
-    env = dict(os.environ, SHUF_FAST_FINISH="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    r = subprocess.run([sys.executable, "-c", _ENV_CASES % root], env=dict(os.environ, **env), capture_output=True,
+                       text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -14,24 +14,41 @@ wl = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else 
 reps = 3
 w = synth.WORKLOADS[wl]
 dev = torch.device("cuda", 0)
-x = synth.make_input_torch(w, dev)
-plan = shuf.shuf_plan(w.n, w.elem_bytes, w.k, w.L, w.seed)
+d_off = None
+if w.kind == "segmented":
+    off = synth.segment_offsets(synth.c5_lengths(w.num_segments, w.seed))
+    n = int(off[-1])
+    x = synth.make_input_torch(w, dev, offsets=off)
+    d_off = torch.as_tensor(off.astype("int64"), device=dev)
+else:
+    n = w.n
+    x = synth.make_input_torch(w, dev)
+plan = shuf.shuf_plan(n, w.elem_bytes, w.k, w.L, w.seed)
 scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
+
+
+def run():
+    if d_off is None:
+        shuf.shuf_run(plan, x, scratch)
+    else:
+        shuf.shuf_segmented(plan, x, d_off, scratch)
+
+
 for _ in range(2):
-    shuf.shuf_run(plan, x, scratch)
+    run()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(reps):
-    shuf.shuf_run(plan, x, scratch)
+    run()
 e1.record()
 torch.cuda.synchronize()
 print(f"{wl}: {e0.elapsed_time(e1) / reps:.3f} ms/shuffle (stream-ordered, no per-launch events)")
-prof = shuf.shuf_profile_run(plan, x, scratch, None)
+prof = shuf.shuf_profile_run(plan, x, scratch, d_off)
 for k, (ms, n) in prof.items():
     print(f"  {k:8s} {ms:8.3f} ms  launches={n}")
 print("device error", shuf.shuf_last_device_error(plan), "env SHUF_FAST_FINISH =", os.environ.get("SHUF_FAST_FINISH"))
-shuf.shuf_run(plan, x, scratch)
+run()
 c = shuf.shuf_debug_clocks(plan)
 if "--scatter" in sys.argv:
     print("scatter CTA 0 level 0 tile phases (cycles): draws+count, wait+sync, scan, place, copyout, total")
