@@ -82,6 +82,31 @@ shuf_status shuf_run(shuf_plan_t p, void *ptr, void *scratch, uint64_t scratch_b
 shuf_status shuf_segmented(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, uint64_t num_segments,
                            void *scratch, uint64_t scratch_bytes, void *stream);
 
+/* In-place mode (the paper's in-place motivation P:32-36,
+ * P:39-43).  Shuffles ptr[0..n) using an auxiliary DEVICE buffer `aux` of
+ * shuf_aux_bytes_inplace() bytes, about 2 bytes per 128-byte block of ptr plus
+ * O(k * 1024 * 128 B) for bucket buffers -- a few percent of n*elem_bytes
+ * instead of shuf_run's n*elem_bytes ping-pong buffer.  Each level longer than
+ * the fused size classifies elements into 128-byte blocks in place, permutes
+ * the blocks into their buckets' regions and fills the bucket heads and tails
+ * from the leftover buffers (the block scheme of in-place samplesort).
+ * Element buckets are the D4 draws at their positions at that level, so the
+ * level-0 bucket contents equal shuf_run's; within a bucket the order depends
+ * on atomics: the result is a uniformly random permutation but NOT
+ * reproducible and NOT equal to shuf_run's.  Segments of at most the fused
+ * size and leaves run the same (deterministic) in-place finish and leaf
+ * kernels as shuf_run.  Host-synchronous: the call synchronises `stream` once
+ * per level (it reads back the next level's segment list to batch it).
+ * ptr and aux must be 16-byte aligned; aux is overwritten; no allocation. */
+shuf_status shuf_aux_bytes_inplace(shuf_plan_t p, uint64_t *bytes);
+shuf_status shuf_run_inplace(shuf_plan_t p, void *ptr, void *aux, uint64_t aux_bytes, void *stream);
+
+/* Test hook: the in-place mode with only levels l < max_levels and leaves
+ * Fisher-Yates'd only if run_leaves != 0 (max_levels = 1, run_leaves = 0
+ * leaves each level-0 bucket, in arbitrary order, at its bucket range). */
+shuf_status shuf_debug_inplace_levels(shuf_plan_t p, void *ptr, void *aux, uint64_t aux_bytes, void *stream,
+                                      uint32_t max_levels, int run_leaves);
+
 /* Test hook: like shuf_run, but only scatter levels l < max_levels run (in
  * HBM or in shared memory alike) and leaves are Fisher-Yates'd only if
  * run_leaves != 0; the state reached is left in ptr.  Equals the oracle's

@@ -35,7 +35,8 @@ EXPORTED_SYMBOLS = [
     "shuf_plan", "shuf_last_status", "shuf_scratch_bytes", "shuf_run", "shuf_segmented", "shuf_debug_run_levels",
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
-    "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks",
+    "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks", "shuf_aux_bytes_inplace", "shuf_run_inplace",
+    "shuf_debug_inplace_levels",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish", "leaf"]
 
@@ -88,6 +89,12 @@ def lib():
         L.shuf_last_run_stats.restype = i32
         L.shuf_debug_clocks.argtypes = [vp, vp, vp, u32]
         L.shuf_debug_clocks.restype = i32
+        L.shuf_aux_bytes_inplace.argtypes = [vp, ctypes.POINTER(u64)]
+        L.shuf_aux_bytes_inplace.restype = i32
+        L.shuf_run_inplace.argtypes = [vp, vp, vp, u64, vp]
+        L.shuf_run_inplace.restype = i32
+        L.shuf_debug_inplace_levels.argtypes = [vp, vp, vp, u64, vp, u32, i32]
+        L.shuf_debug_inplace_levels.restype = i32
         L.shuf_rank_mode.restype = i32
         L.shuf_status_string.argtypes = [i32]
         L.shuf_status_string.restype = ctypes.c_char_p
@@ -183,6 +190,26 @@ def shuf_segmented(plan: Plan, x, d_offsets, scratch, stream=None):
                                 _stream(stream)), "shuf_segmented", plan)
 
 
+def shuf_aux_bytes_inplace(plan: Plan) -> int:
+    v = ctypes.c_uint64(0)
+    _check(lib().shuf_aux_bytes_inplace(plan.handle, ctypes.byref(v)), "shuf_aux_bytes_inplace", plan)
+    return int(v.value)
+
+
+def shuf_run_inplace(plan: Plan, x, aux, stream=None):
+    """In-place mode (not reproducible; synchronises the stream once per level)."""
+    _check_data(plan, x)
+    _check(lib().shuf_run_inplace(plan.handle, _dev_ptr(x, "x"), _dev_ptr(aux, "aux"), aux.numel() * aux.element_size(),
+                                  _stream(stream)), "shuf_run_inplace", plan)
+
+
+def shuf_debug_inplace_levels(plan: Plan, x, aux, max_levels: int, run_leaves: bool, stream=None):
+    _check_data(plan, x)
+    _check(lib().shuf_debug_inplace_levels(plan.handle, _dev_ptr(x, "x"), _dev_ptr(aux, "aux"),
+                                           aux.numel() * aux.element_size(), _stream(stream), max_levels,
+                                           1 if run_leaves else 0), "shuf_debug_inplace_levels", plan)
+
+
 def shuf_debug_run_levels(plan: Plan, x, scratch, max_levels: int, run_leaves: bool, stream=None):
     _check_data(plan, x)
     _check(lib().shuf_debug_run_levels(plan.handle, _dev_ptr(x, "x"), _dev_ptr(scratch, "scratch"),
@@ -258,6 +285,22 @@ def shuffle(x, k: int, L: int, seed: int, elem_bytes: int | None = None, scratch
     err = shuf_last_device_error(plan, stream)
     if err:
         raise ShufError(err, "shuf_run (device)")
+    return x
+
+
+def inplace_shuffle(x, k: int, L: int, seed: int, elem_bytes: int | None = None, aux=None, stream=None):
+    """In-place mode: shuffle the rows of x with an auxiliary buffer of a few
+    percent of x (shuf_aux_bytes_inplace) instead of a full copy."""
+    import torch
+    n = x.shape[0] if x.dim() else 1
+    eb = elem_bytes or (x.numel() * x.element_size() // max(1, n))
+    plan = shuf_plan(n, eb, k, L, seed)
+    if aux is None:
+        aux = torch.empty(max(1, shuf_aux_bytes_inplace(plan)), dtype=torch.uint8, device=x.device)
+    shuf_run_inplace(plan, x, aux, stream)
+    err = shuf_last_device_error(plan, stream)
+    if err:
+        raise ShufError(err, "shuf_run_inplace (device)")
     return x
 
 

@@ -485,6 +485,82 @@ __global__ void __launch_bounds__(NTF, 1) k_finish_children(RunParams rp, LevelP
     run_items<EB, NARROW, ORD>(rp, F, iter, lp.dst);
 }
 
+// Children of an in-place level batch (kernels_inplace.cu): bucket starts
+// from the batch's table S, in place in ptr.  Same protocol as ChildIter.
+struct IpChildIter {
+    const RunParams* rp;
+    const IpParams* ip;
+    uint32_t groups;
+    __device__ __forceinline__ void load_unit(FinCtl* ctl) const {  // warp 0, all lanes
+        const uint32_t lane = threadIdx.x & 31u, k = rp->k;
+        const uint32_t s = (uint32_t)(ctl->u / groups);
+        const uint32_t b0 = (uint32_t)(ctl->u % groups) * kUnit;
+        const uint32_t bend = min(k, b0 + kUnit);
+        if (lane <= bend - b0) ctl->ub[lane] = ip->S[(uint64_t)s * (k + 1) + b0 + lane];
+        if (lane == 0) {
+            ctl->b = b0;
+            ctl->bend = bend;
+            ctl->seg_start = ip->segs[s].start;
+            ctl->seg_origin = 0;
+            ctl->seg_key = rp->seed;  // K(seed, 0) (D2)
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {  // warp 0, all lanes
+        const uint32_t lane = threadIdx.x & 31u;
+        const uint32_t lvl = ip->level + 1;
+        while (ctl->u < ctl->units) {
+            const uint32_t b0 = (uint32_t)(ctl->u % groups) * kUnit;
+            for (uint32_t b = ctl->b; b < ctl->bend; ++b) {
+                const uint64_t s0 = ctl->ub[b - b0], len = ctl->ub[b - b0 + 1] - s0;
+                if (len == 0 || len > rp->S_fuse) continue;
+                if (rp->leafk && len <= rp->L) continue;
+                if (!item_permutes(*rp, (uint32_t)len, lvl)) continue;
+                __syncwarp();
+                if (lane == 0) {
+                    Item& it = ctl->items[slot];
+                    it.start = ctl->seg_start + s0;
+                    it.len = (uint32_t)len;
+                    it.level = lvl;
+                    it.origin = ctl->seg_origin;
+                    it.key = ctl->seg_key;
+                    ctl->have[slot] = 1;
+                    ctl->b = b + 1;
+                }
+                __syncwarp();
+                return;
+            }
+            __syncwarp();
+            if (lane == 0) ctl->u += gridDim.x;
+            __syncwarp();
+            if (ctl->u < ctl->units) load_unit(ctl);
+        }
+        __syncwarp();
+        if (lane == 0) ctl->have[slot] = 0;
+        __syncwarp();
+    }
+};
+
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(NTF, 1) k_finish_ipchildren(RunParams rp, IpParams ip) {
+    const uint32_t groups = (rp.k + kUnit - 1) / kUnit;
+    const uint64_t units = (uint64_t)ip.nseg * groups;
+    if (blockIdx.x >= units) return;
+    const Fin F(rp);
+    fin_init(F);
+    IpChildIter iter{&rp, &ip, groups};
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) {
+            F.ctl()->u = blockIdx.x;
+            F.ctl()->units = units;
+        }
+        __syncwarp();
+        iter.load_unit(F.ctl());
+    }
+    __syncthreads();
+    run_items<EB, NARROW, ORD>(rp, F, iter, rp.buf0);
+}
+
 // Segments given by offsets (segmented mode at level 0, or the single problem
 // when n <= S_fuse).  They sit in ptr.
 struct SegIter {
@@ -583,6 +659,26 @@ cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offset
                             args, smem, s);
 }
 
+template <int EB>
+static void* fin_ip_fn(bool narrow, bool ord) {
+    if (ord) return narrow ? (void*)k_finish_ipchildren<EB, true, true> : (void*)k_finish_ipchildren<EB, false, true>;
+    return narrow ? (void*)k_finish_ipchildren<EB, true, false> : (void*)k_finish_ipchildren<EB, false, false>;
+}
+static void* fin_ip(uint32_t eb, bool narrow, bool ord) {
+    switch (eb) {
+    case 4: return fin_ip_fn<4>(narrow, ord);
+    case 8: return fin_ip_fn<8>(narrow, ord);
+    default: return fin_ip_fn<16>(narrow, ord);
+    }
+}
+
+cudaError_t launch_finish_ipchildren(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
+    const uint32_t smem = finish_smem_bytes(rp.S_fuse, rp.eb, rp.k, 1);
+    void* args[] = {(void*)&rp, (void*)&ip};
+    return cudaLaunchKernel(fin_ip(rp.eb, rp.bp.narrow != 0, rp.rank_ordered != 0), dim3(grid), dim3(NTF), args, smem,
+                            s);
+}
+
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     switch (rp.eb) {
     case 4: k_copy_big<4><<<grid, 256, 0, s>>>(rp, lp); break;
@@ -600,6 +696,9 @@ cudaError_t configure_finish(uint32_t smem) {
                     cudaError_t e = cudaFuncSetAttribute(fin_fn(eb, seg, nr, o),
                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
                     if (e) return e;
+                    if (seg == 0 && (e = cudaFuncSetAttribute(fin_ip(eb, nr, o),
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))
+                        return e;
                 }
     return cudaSuccess;
 }

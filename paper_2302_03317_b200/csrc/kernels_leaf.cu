@@ -102,6 +102,28 @@ struct ItemLeaves {
     }
 };
 
+// Leaf `lane` of unit u of an in-place level batch: children 32g .. 32g+31 of
+// batch segment s (bucket starts from the batch table S), in place.
+struct IpChildLeaves {
+    const IpParams* ip;
+    uint32_t k, groups;
+    uint64_t seed;
+    __device__ __forceinline__ uint64_t units() const { return (uint64_t)ip->nseg * groups; }
+    __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
+        Leaf f{0, 0, 0, 0};
+        const uint32_t s = (uint32_t)(u / groups), b = (uint32_t)(u % groups) * 32u + lane;
+        if (b < k) {
+            const uint64_t* S = ip->S + (uint64_t)s * (k + 1);
+            const uint64_t s0 = S[b], s1 = S[b + 1];
+            f.start = ip->segs[s].start + s0;
+            f.len = s1 - s0;
+            f.origin = 0;
+            f.key = seed;
+        }
+        return f;
+    }
+};
+
 template <int EB, class Src>
 __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned char* src, const Src& ls,
                                            uint32_t slot_bytes) {
@@ -228,8 +250,16 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_items(RunParams rp) {
     run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
 }
 
-// mode: 0 children, 1 segments, 2 items
+template <int EB>
+__global__ void __launch_bounds__(kLeafThreads) k_leaf_ipchildren(RunParams rp, IpParams ip) {
+    const IpChildLeaves ls{&ip, rp.k, (rp.k + 31) / 32, rp.seed};
+    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
+}
+
+// mode: 0 children, 1 segments, 2 items, 3 in-place children
 static void* leaf_fn(uint32_t eb, int mode) {
+    if (mode == 3) return eb == 4 ? (void*)k_leaf_ipchildren<4> : eb == 8 ? (void*)k_leaf_ipchildren<8>
+                                                                        : (void*)k_leaf_ipchildren<16>;
     switch (eb) {
     case 4: return mode == 1 ? (void*)k_leaf_segments<4> : mode == 2 ? (void*)k_leaf_items<4> : (void*)k_leaf_children<4>;
     case 8: return mode == 1 ? (void*)k_leaf_segments<8> : mode == 2 ? (void*)k_leaf_items<8> : (void*)k_leaf_children<8>;
@@ -240,7 +270,7 @@ static void* leaf_fn(uint32_t eb, int mode) {
 
 cudaError_t configure_leaf(uint32_t eb, uint32_t L) {
     const uint32_t smem = leaf_smem_bytes(eb, L);
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
         cudaError_t e = cudaFuncSetAttribute(leaf_fn(eb, mode), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e) return e;
     }
@@ -268,6 +298,11 @@ cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets,
 cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp};
     return cudaLaunchKernel(leaf_fn(rp.eb, 2), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L), s);
+}
+
+cudaError_t launch_leaf_ipchildren(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
+    void* args[] = {(void*)&rp, (void*)&ip};
+    return cudaLaunchKernel(leaf_fn(rp.eb, 3), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L), s);
 }
 
 }  // namespace shuf

@@ -18,17 +18,27 @@
 
 using namespace shuf;
 
+// Byte offsets of the in-place mode's auxiliary buffer (kernels_inplace.cu).
+struct IpAuxLayout {
+    uint64_t header, ctr, segs[2], zseg, N, F, S, wr, ovf, ovfd, pcnt, part, tags, total;
+    uint64_t Z, max_segs;
+    uint32_t cap;
+};
+
 struct shuf_plan_s {
     uint64_t n;
     uint32_t eb, k, L;
     uint64_t seed;
     uint32_t S_fuse, chunk, levels, fin_nbuf;
     ScratchLayout lay;
+    IpAuxLayout ipl;
     // device setup (lazily, first run)
     bool dev_ready;
     int sms;
     int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small, grid_fast, grid_leaf;
     int fast, leafk, defer;
+    bool ip_ready;
+    int grid_ipc, grid_ipp;
     int rank_ordered;
     uint32_t finish_smem, scatter_smem;
     int last_cuda_error;
@@ -114,6 +124,41 @@ static void compute_layout(shuf_plan_s* p) {
     l.total = off;
 }
 
+// In-place aux: batches of <= cap stripes / segments; stripes of Z elements
+// (a multiple of the block and of the classify tile) so that one segment
+// never needs more than cap stripes.
+static void compute_ip_layout(shuf_plan_s* p) {
+    IpAuxLayout& l = p->ipl;
+    const uint64_t n = p->n, k = p->k;
+    const uint64_t B = kIpBlockBytes / p->eb;
+    l.Z = align_up((n + kIpBatchCap - 1) / kIpBatchCap, 4096);
+    if (l.Z < 65536) l.Z = 65536;
+    l.max_segs = n / ((uint64_t)p->S_fuse + 1) + 1;
+    uint64_t cap = n / l.Z + l.max_segs + 1;
+    l.cap = (uint32_t)(cap < kIpBatchCap ? cap : kIpBatchCap);
+    uint64_t off = 0;
+    auto take = [&off](uint64_t bytes) {
+        const uint64_t at = off;
+        off = align_up(off + bytes, 256);
+        return at;
+    };
+    l.header = take(sizeof(Header));
+    l.ctr = take(sizeof(IpCounters));
+    l.segs[0] = take(l.max_segs * sizeof(IpSeg));
+    l.segs[1] = take(l.max_segs * sizeof(IpSeg));
+    l.zseg = take((uint64_t)l.cap * 4);
+    l.N = take((uint64_t)l.cap * k * 8);
+    l.F = take((uint64_t)l.cap * k * 4);
+    l.S = take((uint64_t)l.cap * (k + 1) * 8);
+    l.wr = take((uint64_t)l.cap * k * 8);
+    l.ovf = take((uint64_t)l.cap * k * 4);
+    l.ovfd = take((uint64_t)l.cap * k * kIpBlockBytes);
+    l.pcnt = take((uint64_t)l.cap * k * 4);
+    l.part = take((uint64_t)l.cap * k * kIpBlockBytes);
+    l.tags = take((n / B + 2) * 2);
+    l.total = off;
+}
+
 extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, uint32_t L, uint64_t seed) {
     g_last_status = SHUF_OK;
     if (!(elem_bytes == 4 || elem_bytes == 8 || elem_bytes == 16) && elem_bytes != 0) {
@@ -158,6 +203,7 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     p->chunk = (uint32_t)C;
     p->levels = plan_levels(n, k, S);
     compute_layout(p);
+    compute_ip_layout(p);
     return p;
 }
 
@@ -395,6 +441,164 @@ extern "C" shuf_status shuf_run(shuf_plan_t p, void* ptr, void* scratch, uint64_
         return SHUF_OK;
     }
     return enqueue(p, ptr, nullptr, 0, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
+}
+
+// ------------------------------------------------------------ in-place ---
+extern "C" shuf_status shuf_aux_bytes_inplace(shuf_plan_t p, uint64_t* bytes) {
+    if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    *bytes = p->ipl.total;
+    return SHUF_OK;
+}
+
+// Host-orchestrated level loop of the in-place mode: one stream
+// synchronisation per level (the next level's segment list is read back to
+// cut it into batches of <= cap stripes).
+static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStream_t st, uint32_t max_levels,
+                                   int run_leaves) {
+    p->last_launches = 0;
+    cudaError_t e = device_setup(p);
+    if (e) return cuda_fail(p, e);
+    if (!p->ip_ready) {
+        if ((e = configure_inplace(p->eb, p->k))) return cuda_fail(p, e);
+        if (!p->leafk && (e = configure_leaf(p->eb, p->L))) return cuda_fail(p, e);
+        int oc = 1, op = 1;
+        if ((e = occupancy_inplace(p->eb, p->k, &oc, &op))) return cuda_fail(p, e);
+        p->grid_ipc = p->sms * (oc < 1 ? 1 : oc);
+        p->grid_ipp = p->sms * (op < 1 ? 1 : op);
+        if (p->grid_leaf == 0) {
+            int ol = 1;
+            if ((e = occupancy_leaf(p->eb, p->L, &ol))) return cuda_fail(p, e);
+            p->grid_leaf = p->sms * (ol < 1 ? 1 : ol);
+        }
+        p->ip_ready = true;
+    }
+    const IpAuxLayout& l = p->ipl;
+    unsigned char* ax = static_cast<unsigned char*>(aux);
+    Header* hdr = reinterpret_cast<Header*>(ax + l.header);
+    IpCounters* ctr = reinterpret_cast<IpCounters*>(ax + l.ctr);
+    p->last_hdr = hdr;
+    RunParams rp{};
+    rp.buf0 = static_cast<unsigned char*>(ptr);
+    rp.buf1 = nullptr;
+    rp.hdr = hdr;
+    rp.n = p->n;
+    rp.eb = p->eb;
+    rp.k = p->k;
+    rp.L = p->L;
+    rp.S_fuse = p->S_fuse;
+    rp.chunk = p->chunk;
+    rp.max_levels = max_levels;
+    rp.planned_levels = p->levels;
+    rp.run_leaves = run_leaves;
+    rp.bp = make_bucket_params(p->k);
+    rp.seed = p->seed;
+    rp.rank_ordered = (uint32_t)p->rank_ordered;
+    rp.fin_nbuf = p->fin_nbuf;
+    rp.fast = 0;
+    rp.leafk = 1;
+    rp.defer = 0;
+    rp.items = nullptr;
+    rp.flags = nullptr;
+    rp.dbg = 0;
+    uint64_t launches = 0;
+    Prof* prof = nullptr;
+    if ((e = cudaMemsetAsync(ax, 0, l.segs[0], st))) return cuda_fail(p, e);  // header + counters
+    if ((e = cudaMemsetAsync(ax + l.N, 0, l.S - l.N, st))) return cuda_fail(p, e);  // N, F
+    if ((e = cudaMemsetAsync(ax + l.ovf, 0, l.ovfd - l.ovf, st))) return cuda_fail(p, e);
+    LAUNCH(SHUF_K_INIT, launch_ip_root(hdr, p->n, st));
+    if (p->n <= p->S_fuse) {
+        if (p->n <= p->L) LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, hdr->root_off, 1, st, 1));
+        else LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
+        p->last_launches = launches;
+        return SHUF_OK;
+    }
+    if (max_levels == 0) {
+        p->last_launches = launches;
+        return SHUF_OK;
+    }
+    IpSeg root{0, p->n, 0, 0};
+    IpSeg* segs[2] = {reinterpret_cast<IpSeg*>(ax + l.segs[0]), reinterpret_cast<IpSeg*>(ax + l.segs[1])};
+    if ((e = cudaMemcpyAsync(segs[0], &root, sizeof root, cudaMemcpyHostToDevice, st))) return cuda_fail(p, e);
+    uint32_t nseg = 1, cur = 0;
+    std::vector<IpSeg> hs;
+    for (uint32_t lv = 0; nseg > 0; ++lv) {
+        if (lv >= kMaxLevels) return SHUF_ERR_DEPTH;
+        hs.resize(nseg);
+        if ((e = cudaMemcpyAsync(hs.data(), segs[cur], nseg * sizeof(IpSeg), cudaMemcpyDeviceToHost, st)))
+            return cuda_fail(p, e);
+        if ((e = cudaMemsetAsync(&ctr->nnext[cur ^ 1u], 0, 4, st))) return cuda_fail(p, e);
+        if ((e = cudaStreamSynchronize(st))) return cuda_fail(p, e);
+        for (uint32_t s0 = 0; s0 < nseg;) {
+            uint32_t s1 = s0, nz = 0;
+            while (s1 < nseg && s1 - s0 < l.cap) {
+                const uint32_t z = (uint32_t)((hs[s1].len + l.Z - 1) / l.Z);
+                if (s1 > s0 && nz + z > l.cap) break;
+                nz += z;
+                ++s1;
+            }
+            IpParams ip;
+            ip.segs = segs[cur] + s0;
+            ip.nseg = s1 - s0;
+            ip.nstripes = nz;
+            ip.level = lv;
+            ip.pad = 0;
+            ip.Z = l.Z;
+            ip.zseg = reinterpret_cast<uint32_t*>(ax + l.zseg);
+            ip.N = reinterpret_cast<uint64_t*>(ax + l.N);
+            ip.F = reinterpret_cast<uint32_t*>(ax + l.F);
+            ip.S = reinterpret_cast<uint64_t*>(ax + l.S);
+            ip.wr = reinterpret_cast<uint64_t*>(ax + l.wr);
+            ip.ovf = reinterpret_cast<uint32_t*>(ax + l.ovf);
+            ip.ovfd = ax + l.ovfd;
+            ip.pcnt = reinterpret_cast<uint32_t*>(ax + l.pcnt);
+            ip.part = ax + l.part;
+            ip.tags = reinterpret_cast<uint16_t*>(ax + l.tags);
+            ip.next = segs[cur ^ 1u];
+            ip.nnext = &ctr->nnext[cur ^ 1u];
+            ip.max_next = l.max_segs;
+            ip.cursor = &ctr->cursor;
+            if ((e = cudaMemsetAsync(&ctr->cursor, 0, sizeof ctr->cursor, st))) return cuda_fail(p, e);
+            LAUNCH(SHUF_K_PLAN, launch_ip_stripes(ip, st));
+            LAUNCH(SHUF_K_HIST, launch_ip_classify(rp, ip, st, p->grid_ipc));
+            LAUNCH(SHUF_K_PLAN, launch_ip_plan(rp, ip, st));
+            LAUNCH(SHUF_K_SCATTER, launch_ip_permute(rp, ip, st, p->grid_ipp));
+            LAUNCH(SHUF_K_SCAN, launch_ip_fill(rp, ip, st, p->grid_ipp));
+            LAUNCH(SHUF_K_FINISH, launch_finish_ipchildren(rp, ip, st, p->grid_finish));
+            LAUNCH(SHUF_K_LEAF, launch_leaf_ipchildren(rp, ip, st, p->grid_leaf));
+            s0 = s1;
+        }
+        uint32_t nn = 0;
+        if ((e = cudaMemcpyAsync(&nn, &ctr->nnext[cur ^ 1u], 4, cudaMemcpyDeviceToHost, st))) return cuda_fail(p, e);
+        if ((e = cudaStreamSynchronize(st))) return cuda_fail(p, e);
+        if (nn > l.max_segs) return SHUF_ERR_DEPTH;
+        nseg = nn;
+        cur ^= 1u;
+    }
+    p->last_launches = launches;
+    return SHUF_OK;
+}
+
+static shuf_status check_inplace_args(shuf_plan_s* p, void* ptr, void* aux, uint64_t aux_bytes) {
+    if (!p) return SHUF_ERR_INVALID_ARG;
+    if (p->n > 1 && (!ptr || !aux)) return SHUF_ERR_INVALID_ARG;
+    if (((uintptr_t)ptr & 15u) || ((uintptr_t)aux & 15u)) return SHUF_ERR_ALIGNMENT;
+    if (p->n > 1 && aux_bytes < p->ipl.total) return SHUF_ERR_SCRATCH;
+    return SHUF_OK;
+}
+
+extern "C" shuf_status shuf_run_inplace(shuf_plan_t p, void* ptr, void* aux, uint64_t aux_bytes, void* stream) {
+    shuf_status s = check_inplace_args(p, ptr, aux, aux_bytes);
+    if (s) return s;
+    if (p->n <= 1) return SHUF_OK;
+    return enqueue_inplace(p, ptr, aux, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
+}
+
+extern "C" shuf_status shuf_debug_inplace_levels(shuf_plan_t p, void* ptr, void* aux, uint64_t aux_bytes,
+                                                 void* stream, uint32_t max_levels, int run_leaves) {
+    shuf_status s = check_inplace_args(p, ptr, aux, aux_bytes);
+    if (s) return s;
+    if (p->n <= 1) return SHUF_OK;
+    return enqueue_inplace(p, ptr, aux, static_cast<cudaStream_t>(stream), max_levels, run_leaves ? 1 : 0);
 }
 
 extern "C" shuf_status shuf_debug_run_levels(shuf_plan_t p, void* ptr, void* scratch, uint64_t scratch_bytes,

@@ -19,6 +19,8 @@ constexpr uint32_t kSegGroup = 8;          // user segments per finish work unit
 constexpr uint32_t kMaxLevels = 256;
 constexpr uint32_t kScatterTileBytes = 24576; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
 constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
+constexpr uint32_t kIpBlockBytes = 128;     // in-place mode block (kernels_inplace.cu)
+constexpr uint32_t kIpBatchCap = 1024;      // in-place mode: stripes (and segments) per batch
 
 // ---------------------------------------------------------- descriptors ---
 // A segment processed by an HBM-resident ("global") scatter level.
@@ -127,6 +129,43 @@ struct LevelParams {
     unsigned char* dst;  // level output buffer
 };
 
+// ------------------------------------------------------- in-place mode ---
+// A segment of an in-place HBM level (kernels_inplace.cu); zbase/nz: its
+// stripes within the batch.
+struct IpSeg {
+    uint64_t start, len;
+    uint32_t zbase, nz;
+};
+
+struct IpCounters {
+    uint32_t nnext[2];  // next-level list lengths (by level parity)
+    unsigned long long cursor;  // k_ip_permute pair cursor
+};
+
+// One batch of segments of one in-place level.
+struct IpParams {
+    IpSeg* segs;              // the batch's segments
+    uint32_t nseg;            // segments in the batch
+    uint32_t nstripes;        // stripes in the batch
+    uint32_t level;
+    uint32_t pad;
+    uint64_t Z;               // stripe length (elements, multiple of the block)
+    uint32_t* zseg;           // stripe -> batch segment
+    uint64_t* N;              // [nseg*k] elements per (segment, bucket)
+    uint32_t* F;              // [nseg*k] full blocks per (segment, bucket)
+    uint64_t* S;              // [nseg*(k+1)] bucket starts (segment-relative)
+    uint64_t* wr;             // [nseg*k] packed (write << 32 | read + 2^31) block pointers
+    uint32_t* ovf;            // [nseg*k] 1: the overflow block of (segment, bucket) is used
+    unsigned char* ovfd;      // [nseg*k] overflow blocks
+    uint32_t* pcnt;           // [nstripes*k] partial counts
+    unsigned char* part;      // [nstripes*k] partial buffers (one block each)
+    uint16_t* tags;           // per block slot: bucket / empty / read
+    IpSeg* next;              // next level's list
+    uint32_t* nnext;
+    uint64_t max_next;
+    unsigned long long* cursor;
+};
+
 // ------------------------------------------------------ host launchers ---
 cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid);
 cudaError_t launch_init_segmented(const RunParams& rp, const LevelParams& lp0, const uint64_t* d_offsets,
@@ -152,6 +191,17 @@ cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid);
 cudaError_t configure_leaf(uint32_t eb, uint32_t L);
 cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks);
 uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L);
+cudaError_t launch_ip_root(Header* hdr, uint64_t n, cudaStream_t s);
+cudaError_t launch_ip_stripes(const IpParams& ip, cudaStream_t s);
+cudaError_t launch_ip_classify(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
+cudaError_t launch_ip_plan(const RunParams& rp, const IpParams& ip, cudaStream_t s);
+cudaError_t launch_ip_permute(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
+cudaError_t launch_ip_fill(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
+cudaError_t launch_finish_ipchildren(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
+cudaError_t launch_leaf_ipchildren(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
+cudaError_t configure_inplace(uint32_t eb, uint32_t k);
+cudaError_t occupancy_inplace(uint32_t eb, uint32_t k, int* classify, int* permute);
+uint32_t ip_classify_smem_bytes(uint32_t eb, uint32_t k);
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);

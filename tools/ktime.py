@@ -27,8 +27,14 @@ plan = shuf.shuf_plan(n, w.elem_bytes, w.k, w.L, w.seed)
 scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
 
 
+INPLACE = "--inplace" in sys.argv
+aux = torch.empty(max(1, shuf.shuf_aux_bytes_inplace(plan)), dtype=torch.uint8, device=dev) if INPLACE else None
+
+
 def run():
-    if d_off is None:
+    if INPLACE:
+        shuf.shuf_run_inplace(plan, x, aux)
+    elif d_off is None:
         shuf.shuf_run(plan, x, scratch)
     else:
         shuf.shuf_segmented(plan, x, d_off, scratch)
@@ -43,7 +49,11 @@ for _ in range(reps):
     run()
 e1.record()
 torch.cuda.synchronize()
-print(f"{wl}: {e0.elapsed_time(e1) / reps:.3f} ms/shuffle (stream-ordered, no per-launch events)")
+print(f"{wl}: {e0.elapsed_time(e1) / reps:.3f} ms/shuffle (stream-ordered, no per-launch events)"
+      + (" IN-PLACE" if INPLACE else ""))
+if INPLACE:
+    print("aux MiB", shuf.shuf_aux_bytes_inplace(plan) / 2**20, "device error", shuf.shuf_last_device_error(plan))
+    sys.exit(0)
 prof = shuf.shuf_profile_run(plan, x, scratch, d_off)
 for k, (ms, n) in prof.items():
     print(f"  {k:8s} {ms:8.3f} ms  launches={n}")
