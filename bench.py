@@ -223,7 +223,8 @@ def main():
     peaks, peak_src = load_peaks()
     hbm_peak = float(peaks["hbm_gbs"])
     eb = w.elem_bytes
-    kbytes = {"scatter": 2 * eb * sum(stats["scattered_hbm"]), "finish": 2 * eb * stats["finished"]}
+    kbytes = {"scatter": 2 * eb * sum(stats["scattered_hbm"]), "finish": 2 * eb * stats["finished"],
+              "leaf": 2 * eb * stats.get("leafed", 0)}
     kernels = {}
     for name, (kms, cnt) in prof.items():
         d = {"ms": round(kms, 4), "launches": cnt}
@@ -231,7 +232,7 @@ def main():
             d["algorithmic_bytes"] = kbytes[name]
             d["GBps"] = round(kbytes[name] / (kms / 1e3) / 1e9, 1)
         kernels[name] = d
-    dom = max(("scatter", "finish"), key=lambda c: prof[c][0])
+    dom = max(("scatter", "finish", "leaf"), key=lambda c: prof[c][0])
     dms, dcnt = prof[dom]
     achieved = kbytes[dom] / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     traffic = None
