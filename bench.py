@@ -97,6 +97,28 @@ def workload_bytes(w, stats):
     return 2 * w.elem_bytes * (scattered + w.n), scattered
 
 
+# ---- multi-rank host logic (replicas only); tested with gloo on CPU
+def rank_seed(seed: int, rank: int) -> int:
+    """Every rank shuffles its own independent problem."""
+    return seed + rank
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """The job's time is the slowest rank's (all-reduce MAX; nccl on GPU, gloo on CPU)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(n: int, world: int, ms_per_step: float) -> float:
+    """Whole-job throughput: elements of all ranks per second of the slowest rank."""
+    return n * world / (ms_per_step / 1e3)
+
+
 def run_reference(args, rank):
     """--impl reference: the CPU oracle as it stands, bounded sample per step."""
     if rank != 0:
@@ -164,7 +186,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     w = synth.WORKLOADS[args.workload]
-    seed = w.seed + rank
+    seed = rank_seed(w.seed, rank)
     if w.kind == "segmented":
         lens = synth.c5_lengths(w.num_segments, w.seed)
         off_np = synth.segment_offsets(lens)
@@ -208,13 +230,9 @@ def main():
             step()
         e1.record(stream)
         barrier()
-    ms_total = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(e0.elapsed_time(e1), world, dev)
     ms = ms_total / args.steps
-    value = w.n * world / (ms / 1e3)
+    value = job_value(w.n, world, ms)
     eff_bytes, scattered = workload_bytes(w, stats)
     eff_gbps = eff_bytes / (ms / 1e3) / 1e9
 
@@ -264,12 +282,8 @@ def main():
             host_out.copy_(x, non_blocking=True)
         f1.record(stream)
         barrier()
-        e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": w.n * world / (e2e_ms / 1e3), "unit": "elements/s", "ms_per_step": e2e_ms,
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
+        e2e = {"value": job_value(w.n, world, e2e_ms), "unit": "elements/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
         del host_in, host_out
 
