@@ -214,8 +214,12 @@ __device__ __forceinline__ void fy_leaf(unsigned char* el, uint32_t c, uint32_t 
     if (cm < 2) return;
     E* A = reinterpret_cast<E*>(el) + c;
     const uint32_t gt = (cm - 1) >> 3;
+    // the next group's Philox block is computed one group ahead so that its
+    // ALU latency overlaps the current group's swaps
+    uint4 wn = fy16_group_words(key, q, gt);
     {  // top group: steps cm-1 .. max(8*gt, 1)
-        const uint4 w = fy16_group_words(key, q, gt);
+        const uint4 w = wn;
+        if (gt >= 1) wn = fy16_group_words(key, q, gt - 1);
         const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int32_t jj = 7; jj >= 0; --jj) {
@@ -224,16 +228,15 @@ __device__ __forceinline__ void fy_leaf(unsigned char* el, uint32_t c, uint32_t 
         }
     }
     for (int32_t g = (int32_t)gt - 1; g >= 1; --g) {  // full groups
-        const uint4 w = fy16_group_words(key, q, (uint32_t)g);
+        const uint4 w = wn;
+        wn = fy16_group_words(key, q, (uint32_t)g - 1u);
         const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-        E* Ag = A;
 #pragma unroll
         for (int32_t jj = 7; jj >= 0; --jj)
-            fy_step(Ag, (uint32_t)g * 8u + (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+            fy_step(A, (uint32_t)g * 8u + (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
     }
     if (gt >= 1) {  // group 0: steps 7 .. 1
-        const uint4 w = fy16_group_words(key, q, 0u);
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+        const uint32_t wv[4] = {wn.x, wn.y, wn.z, wn.w};
 #pragma unroll
         for (int32_t jj = 7; jj >= 1; --jj) fy_step(A, (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
     }

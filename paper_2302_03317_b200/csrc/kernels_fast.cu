@@ -1,30 +1,24 @@
-// Fast fused finish for the common shape of the recursion (SURVEY 8(a) a7+a8):
-// a child of the last HBM level ("item") that needs exactly ONE more scatter
-// level, after which every grandchild is a leaf (<= L and <= 256 elements)
-// -- e.g. the HOT run's 65 536 children of ~16 K u32 that split into
-// ~64-element leaves.
+// Pipelined fused finish for the common shape of the recursion (SURVEY 8(a)
+// a7+a8): a child of the last HBM level ("item") that needs exactly ONE more
+// scatter level, after which every grandchild is a leaf -- e.g. the HOT
+// run's 65 536 children of ~16 K u32 that split into ~64-element leaves.
 //
-// One CTA of 1024 threads per SM and two item buffers whose roles alternate
-// (DESIGN.md 6.3).  Item t arrives (bulk async copy, TMA engine) in buffer
-// I = t & 1; per item, in phases separated by CTA barriers:
-//   1. draws + counts: the level's bucket draws (D4, Philox) -> shared
-//      memory; warp w owns a run of Philox groups and counts them per bucket;
-//   2. scan: bucket (= leaf) starts, 32-leaf column groups, per-warp row
-//      bases;  (the load of item t has been in flight since item t-1)
-//   3. placement I -> C (the other buffer) in COLUMN layout: leaf b's r-th
-//      element at C[32 (G(b) + r) + (b & 31)]; warp w walks its elements in
-//      rounds of 32 in position order and one ordered shared atomic on its
-//      own table returns the row (stable, D6);
-//   4. Fisher-Yates partners of every leaf (D5), all threads;
-//   5. Fisher-Yates (Fig. 1), one thread per leaf (warps 0..7):
-//      the 32 leaves of a warp sit in 32 banks of C, so each step's loads and
-//      store are conflict-free; position i is final after step i and goes
-//      straight to the contiguous item layout in I (the input is dead);
-//   6. one bulk async store of I to ptr; the load of item t+1 into C (free
-//      again) is issued.
-// Items of another shape (a grandchild > L or > 256 elements, a leaf-only
-// child, more than SMAX elements, column overflow) are flagged and finished
-// by the general kernel (kernels_finish.cu) right after.
+// The general finish (kernels_finish.cu) runs each item's phases back to
+// back with the whole CTA: while one thread per leaf runs Fisher-Yates, three
+// quarters of the CTA wait at a barrier.  Here the CTA is
+// split into three warp groups that work on different items at once, with
+// two item buffers and mbarrier hand-offs (no CTA-wide barrier in the loop):
+//   S (warps 9..31, 736 threads): item t+1 -- draws (D4) + per-warp counts,
+//       bucket starts and per-warp bases, then the stable in-place scatter
+//       inside its buffer (every thread holds its elements in registers
+//       across a group barrier; one ordered shared atomic per element
+//       returns its slot);
+//   F (warps 0..7, 256 threads): item t -- Fisher-Yates (Fig. 1)
+//       of every leaf, one thread per leaf, in place (D5 draws);
+//   C (warp 8): stores item t (bulk async copy, TMA engine) once F is done,
+//       finds the next item and loads it into the freed buffer.
+// Items of another shape (a grandchild > L, a leaf-only child, more than
+// SMAX elements) are flagged and finished by the general kernel right after.
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -36,16 +30,20 @@ namespace shuf {
 
 extern __shared__ __align__(16) unsigned char xsm[];
 
-constexpr int XNT = 1024;          // threads per CTA
-constexpr uint32_t XW = XNT / 32;  // 32 warps: draws, counts, placement
-constexpr uint32_t XFYT = 256;     // Fisher-Yates threads (warps 0..7)
-constexpr uint32_t XBUF = 86016;   // bytes per item buffer (contiguous item / column layout)
-constexpr uint32_t XIN = 69632;    // bytes of the largest item the fast path takes (68 KiB)
+constexpr int XNT = 1024;
+constexpr uint32_t XF = 256;             // F: threads 0..255
+constexpr uint32_t XC = 256;             // C: warp 8 (threads 256..287)
+constexpr uint32_t XS0 = 288;            // S: threads 288..1023
+constexpr uint32_t XSN = XNT - XS0;      // 736
+constexpr uint32_t XSW = XSN / 32;       // 23 warps
+constexpr uint32_t XBUF = 71680;         // bytes per item buffer (70 KiB)
+constexpr uint32_t XIN = XBUF - 16;      // largest item in bytes (alignment slack)
+constexpr uint32_t kBarS = 1, kBarF = 2; // named barriers
 
 template <int EB>
 struct XCfg {
-    static constexpr uint32_t SMAX = XIN / EB;               // largest item
-    static constexpr uint32_t COLCAP = XBUF / EB / 32 * 32;  // column-layout capacity (elements)
+    static constexpr uint32_t SMAX = XIN / EB;                         // largest item
+    static constexpr uint32_t R = (SMAX + 16 * XSW) / (32 * XSW) + 2;  // rounds per S warp
 };
 
 uint32_t fast_max_elems(uint32_t eb) { return XIN / eb; }
@@ -57,18 +55,16 @@ struct XItem {
 };
 
 struct XCtl {
-    XItem cur, nxt, nxt2;  // item t, t+1 (counted during FY(t)), t+2 (searched during FY(t))
-    uint64_t bar[2];  // mbarriers of the two buffers' loads
-    uint32_t ph[2];   // their parities
-    uint32_t cursor;  // this CTA's next candidate child index
-    uint32_t defer;   // cur is handed to the general kernel
-    uint32_t gh[33];  // per 32-leaf group: longest leaf
-    uint32_t dbg_it;  // items processed (phase clocks of the first ones, CTA 0)
+    XItem item[2];
+    uint64_t full[2], ready[2], fydone[2];  // mbarriers per buffer
+    uint32_t defer[2];
+    uint32_t cursor;
+    uint32_t dbg_s, dbg_f;
     unsigned long long st_fin, st_fy;
 };
 
 struct XLayout {
-    uint32_t buf0, buf1, draws, jb, T, meta, wsum, total, jbbytes;
+    uint32_t buf0, buf1, draws, T, perm, bst0, bst1, wsum, total;
 };
 
 __host__ __device__ inline XLayout fast_layout(uint32_t eb, uint32_t k) {
@@ -85,27 +81,45 @@ __host__ __device__ inline XLayout fast_layout(uint32_t eb, uint32_t k) {
     f.buf0 = take(XBUF);
     f.buf1 = take(XBUF);
     f.draws = take((narrow ? 1u : 2u) * (smax + 64));
-    f.jbbytes = XBUF / eb + ((k + 31) / 32 + 1) * 256;  // partner words, column layout (4 steps per word)
-    f.jb = take(f.jbbytes);
-    f.T = take(XW * ((k + 1) / 2) * 4);
-    f.meta = take(((k + 1) + 33 + 33) * 4);  // bst[k+1], gb[33], gj[33]
-    f.wsum = take((XNT / 32 + 1) * 4);
+    f.T = take(XSW * (narrow ? k : (k + 1) / 2) * 4);  // narrow: u32 counters, else packed u16
+    f.perm = take(2 * k * 2);                           // per buffer: FY thread -> leaf
+    f.bst0 = take((k + 1) * 4);
+    f.bst1 = take((k + 1) * 4);
+    f.wsum = take((XSW + 2 + 32) * 4);
     f.total = off;
     return f;
 }
 
 uint32_t fast_smem_bytes(uint32_t eb, uint32_t k) { return fast_layout(eb, k).total; }
 
-// 4-byte asynchronous global -> shared copy (the unaligned head/tail words of
-// an item; completion by cp.async.wait_all).
-__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+__device__ __forceinline__ void bar_group(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
-// Warp element ranges.  The item's positions [P0, P0+m) cover ng Philox
-// groups of dpg draws; warp w owns groups [w*qg, (w+1)*qg), i.e. elements
-// e in [w*qg*dpg - doff, (w+1)*qg*dpg - doff) clipped to [0, m).
+// Exclusive sum over the S group (one value per S thread; sid = 0..XSN-1).
+__device__ __forceinline__ uint32_t s_exclusive_sum(uint32_t v, uint32_t* wsum, uint32_t* total, uint32_t sid) {
+    const uint32_t lane = sid & 31u, warp = sid >> 5;
+    const uint32_t incl = warp_inclusive_sum(v);
+    if (lane == 31) wsum[warp] = incl;
+    bar_group(kBarS, XSN);
+    if (warp == 0) {
+        const uint32_t x = lane < XSW ? wsum[lane] : 0u;
+        const uint32_t xi = warp_inclusive_sum(x);
+        if (lane < XSW) wsum[lane] = xi - x;
+        if (lane == XSW - 1) wsum[XSW] = xi;
+    }
+    bar_group(kBarS, XSN);
+    const uint32_t r = wsum[warp] + incl - v;
+    *total = wsum[XSW];
+    bar_group(kBarS, XSN);
+    return r;
+}
+
+// Warp element ranges of the S group: the item's positions [P0, P0+m)
+// cover ng Philox groups of dpg draws; S warp w owns groups [w*qg, (w+1)*qg).
 template <bool NARROW>
 struct XRange {
     static constexpr uint32_t sh = NARROW ? 4u : 3u, dpg = 1u << sh;
@@ -116,12 +130,11 @@ struct XRange {
         g0 = P0 >> sh;
         doff = (uint32_t)(P0 & (dpg - 1));
         ng = (uint32_t)(((P0 + m - 1) >> sh) - g0 + 1);
-        qg = (ng + XW - 1) / XW;
+        qg = (ng + XSW - 1) / XSW;
     }
 };
 
 // Child c = s*k + b of the level's segments: [start, start+len).
-// (c < 2^32: nseg * k <= max_segs * k is bounded by the scratch layout.)
 __device__ __forceinline__ void child_of(const LevelParams& lp, uint32_t k, uint32_t c, uint64_t& start, uint64_t& len,
                                          SegDesc& sg) {
     sg = lp.segs[c / k];
@@ -147,6 +160,7 @@ __device__ __forceinline__ XItem find_next(const RunParams& rp, const LevelParam
         child_of(lp, rp.k, c, start, len, sg);
         if (len == 0 || len > rp.S_fuse) continue;  // empty, or an HBM segment of the next level
         const bool leaf = len <= rp.L;
+        if (leaf && rp.leafk) continue;             // the leaf kernel's
         const bool permutes = (!leaf && lvl < rp.max_levels) || (leaf && rp.run_leaves && len >= 2);
         if (!permutes) {  // nothing to do unless it must be copied to ptr
             rp.flags[c] = (lp.dst == rp.buf0) ? 0 : 1;
@@ -170,7 +184,6 @@ __device__ __forceinline__ XItem find_next(const RunParams& rp, const LevelParam
     return it;
 }
 
-// Shared-memory views (byte offsets into the dynamic window).
 template <int EB>
 struct XView {
     XLayout Ly;
@@ -179,67 +192,103 @@ struct XView {
     __device__ __forceinline__ XCtl* ctl() const { return reinterpret_cast<XCtl*>(xsm); }
     __device__ __forceinline__ unsigned char* buf(uint32_t i) const { return xsm + (i ? Ly.buf1 : Ly.buf0); }
     __device__ __forceinline__ unsigned char* draws() const { return xsm + Ly.draws; }
-    __device__ __forceinline__ uint32_t* jb() const { return reinterpret_cast<uint32_t*>(xsm + Ly.jb); }
     __device__ __forceinline__ uint32_t* T() const { return reinterpret_cast<uint32_t*>(xsm + Ly.T); }
-    __device__ __forceinline__ uint32_t* bst() const { return reinterpret_cast<uint32_t*>(xsm + Ly.meta); }
-    __device__ __forceinline__ uint32_t* gb() const { return bst() + k + 1; }       // element rows of group g
-    __device__ __forceinline__ uint32_t* gj() const { return bst() + k + 1 + 33; }  // partner-word rows of group g
+    __device__ __forceinline__ uint32_t* bst(uint32_t i) const {
+        return reinterpret_cast<uint32_t*>(xsm + (i ? Ly.bst1 : Ly.bst0));
+    }
     __device__ __forceinline__ uint32_t* wsum() const { return reinterpret_cast<uint32_t*>(xsm + Ly.wsum); }
+    __device__ __forceinline__ uint16_t* perm(uint32_t i) const {
+        return reinterpret_cast<uint16_t*>(xsm + Ly.perm) + i * k;
+    }
 };
 
-// Element e of an item in contiguous layout sits at byte ((start*EB) & 15) +
-// e*EB of its buffer, so the 16-byte-aligned body maps to an aligned address.
+// Element e of an item sits at byte ((start*EB) & 15) + e*EB of its buffer,
+// so the 16-byte-aligned body of the item maps to an aligned address.
 template <int EB>
 __device__ __forceinline__ unsigned char* item_base(unsigned char* buf, uint64_t start) {
     return buf + ((start * EB) & 15u);
 }
 
-// The load of item `it` into buffer bi: the aligned body by one bulk async
-// copy (thread 0), the <= 3 unaligned words at each end by 4-byte
-// asynchronous copies (threads 32..39, which wait for them before phase 3).
+// ---------------------------------------------------------------- C ------
+// Store item `it` from buffer bi (warp C; lane 0 the bulk body, lanes 1..6
+// the <= 3 unaligned words at each end); returns when the buffer is free.
 template <int EB>
-__device__ __forceinline__ void issue_load(const XView<EB>& V, const XItem& it, const unsigned char* src, uint32_t bi) {
-    const uint32_t tid = threadIdx.x;
+__device__ __forceinline__ void c_store(const RunParams& rp, const XView<EB>& V, const XItem& it, uint32_t bi) {
+    const uint32_t lane = threadIdx.x & 31u;
     const uint64_t x0 = it.start * EB, x1 = (it.start + it.len) * EB;
     const uint64_t fl = x0 & ~15ull;
     const uint64_t A = (x0 + 15) & ~15ull, B = x1 & ~15ull;
     const bool body = B > A;
-    unsigned char* buf = V.buf(bi);
-    XCtl* ctl = V.ctl();
-    if (tid == 0) {
+    const unsigned char* ob = V.buf(bi);
+    if (lane == 0 && body) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(&ctl->bar[bi], body ? (uint32_t)(B - A) : 0u);
-        if (body) bulk_g2s(buf + (A - fl), src + A, (uint32_t)(B - A), &ctl->bar[bi]);
-        return;
+        bulk_s2g(rp.buf0 + A, ob + (A - fl), (uint32_t)(B - A));
+        bulk_commit();
     }
-    const uint64_t hEnd = body ? A : x1;
-    const uint32_t nh = (uint32_t)((hEnd - x0) >> 2);
-    const uint64_t tBeg = body ? B : x1;
-    const uint32_t nt = (uint32_t)((x1 - tBeg) >> 2);
-    const uint32_t r = tid - 32;  // 0..7
-    if (r < 4) {
-        if (r < nh) cp_async4(buf + (x0 - fl) + 4 * r, src + x0 + 4 * r);
-    } else if (r - 4 < nt) {
-        cp_async4(buf + (tBeg - fl) + 4 * (r - 4), src + tBeg + 4 * (r - 4));
-    }
+    const uint64_t hEnd = body ? A : x1, tBeg = body ? B : x1;
+    const uint32_t nh = (uint32_t)((hEnd - x0) >> 2), nt = (uint32_t)((x1 - tBeg) >> 2);
+    if (lane >= 1 && lane <= 3 && lane - 1 < nh)
+        *reinterpret_cast<uint32_t*>(rp.buf0 + x0 + 4 * (lane - 1)) =
+            *reinterpret_cast<const uint32_t*>(ob + (x0 - fl) + 4 * (lane - 1));
+    if (lane >= 4 && lane <= 6 && lane - 4 < nt)
+        *reinterpret_cast<uint32_t*>(rp.buf0 + tBeg + 4 * (lane - 4)) =
+            *reinterpret_cast<const uint32_t*>(ob + (tBeg - fl) + 4 * (lane - 4));
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
 }
 
-// ---- phase 1: draws of the item -> smem (indexed by Philox group) and each
-// warp's bucket counts (its groups are its elements).
-// Warps [w0, w0 + nw) do it for all 32 placing warps' ranges (w = w0 + i,
-// w0 + i + nw, ...).
-template <int EB, bool NARROW>
-__device__ __forceinline__ void draw_count_phase(const RunParams& rp, const XView<EB>& V, const XItem& it,
-                                                 uint32_t lvl, uint32_t w0, uint32_t nw) {
-    const uint32_t k = rp.k, kw = (k + 1) >> 1;
+// Find the next item, record it for buffer bi and start its load (warp C).
+template <int EB>
+__device__ __forceinline__ void c_load_next(const RunParams& rp, const LevelParams& lp, const XView<EB>& V,
+                                            uint32_t nchild, uint32_t bi) {
     const uint32_t lane = threadIdx.x & 31u;
+    XCtl* ctl = V.ctl();
+    if (lane == 0) ctl->item[bi] = find_next<EB>(rp, lp, nchild, ctl->cursor);
+    __syncwarp();
+    const XItem it = ctl->item[bi];
+    unsigned char* buf = V.buf(bi);
+    const unsigned char* src = lp.dst;
+    uint32_t bytes = 0;
+    uint64_t A = 0, fl = 0;
+    if (it.valid) {
+        const uint64_t x0 = it.start * EB, x1 = (it.start + it.len) * EB;
+        fl = x0 & ~15ull;
+        A = (x0 + 15) & ~15ull;
+        const uint64_t B = x1 & ~15ull;
+        const bool body = B > A;
+        bytes = body ? (uint32_t)(B - A) : 0u;
+        const uint64_t hEnd = body ? A : x1, tBeg = body ? B : x1;
+        const uint32_t nh = (uint32_t)((hEnd - x0) >> 2), nt = (uint32_t)((x1 - tBeg) >> 2);
+        if (lane >= 1 && lane <= 3 && lane - 1 < nh)
+            *reinterpret_cast<uint32_t*>(buf + (x0 - fl) + 4 * (lane - 1)) =
+                *reinterpret_cast<const uint32_t*>(src + x0 + 4 * (lane - 1));
+        if (lane >= 4 && lane <= 6 && lane - 4 < nt)
+            *reinterpret_cast<uint32_t*>(buf + (tBeg - fl) + 4 * (lane - 4)) =
+                *reinterpret_cast<const uint32_t*>(src + tBeg + 4 * (lane - 4));
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence_block();
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&ctl->full[bi], bytes);
+        if (bytes) bulk_g2s(buf + (A - fl), src + A, bytes, &ctl->full[bi]);
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- S ------
+// Draws of the item -> smem (indexed by Philox group) and each S warp's
+// bucket counts (packed u16 halves).
+template <int EB, bool NARROW>
+__device__ __forceinline__ void s_count(const RunParams& rp, const XView<EB>& V, const XItem& it, uint32_t lvl,
+                                        uint32_t w) {
+    const uint32_t k = rp.k, kw = NARROW ? k : (k + 1) >> 1, lane = threadIdx.x & 31u;
     const BucketParams bp = rp.bp;
     const uint64_t P0 = it.start - it.origin;
     const XRange<NARROW> xr(P0, it.len);
     const uint32_t m = xr.m;
     const PhiloxKey key = make_key(it.key);
     constexpr uint32_t sh = XRange<NARROW>::sh, dpg = XRange<NARROW>::dpg;
-    for (uint32_t w = (threadIdx.x >> 5) - w0; w < XW; w += nw) {
     uint32_t* Tw = V.T() + w * kw;
     for (uint32_t i = lane; i < kw; i += 32) Tw[i] = 0;
     __syncwarp();
@@ -266,364 +315,299 @@ __device__ __forceinline__ void draw_count_phase(const RunParams& rp, const XVie
         *reinterpret_cast<uint4*>(V.draws() + (size_t)t * 16) = packed;
         const int32_t e0 = (int32_t)(t * dpg) - (int32_t)xr.doff;
         const uint32_t pw4[4] = {packed.x, packed.y, packed.z, packed.w};
-        // counter of bucket b: 16-bit half (b & 1) of word b >> 1 of the warp's table
-        if (e0 >= 0 && e0 + (int32_t)dpg <= (int32_t)m) {  // whole group (all but <= 2 per item)
+        if (e0 >= 0 && e0 + (int32_t)dpg <= (int32_t)m) {
 #pragma unroll
             for (uint32_t j = 0; j < dpg; ++j) {
                 const uint32_t b = NARROW ? __byte_perm(pw4[j >> 2], 0u, 0x4440u | (j & 3u))
                                           : (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
-                atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
+                if (NARROW) atomicAdd(&Tw[b], 1u);
+                else atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
             }
         } else {
             for (uint32_t j = 0; j < dpg; ++j) {
                 const int32_t e = e0 + (int32_t)j;
                 const uint32_t b =
                     NARROW ? (pw4[j >> 2] >> ((j & 3u) * 8u)) & 0xFFu : (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
-                if (e >= 0 && e < (int32_t)m) atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
+                if (e >= 0 && e < (int32_t)m) {
+                    if (NARROW) atomicAdd(&Tw[b], 1u);
+                    else atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
+                }
             }
         }
     }
-    }
 }
 
-// ---- phase 2: bucket starts, 32-leaf column groups (element rows gb and
-// partner-word rows gj), per-warp row bases; flags the item for the general
-// kernel if it does not fit.
-template <int EB>
-__device__ __forceinline__ void scan_phase(const RunParams& rp, const XView<EB>& V) {
-    const uint32_t k = rp.k, kw = (k + 1) >> 1;
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    XCtl* ctl = V.ctl();
+// Bucket starts -> bst (k+1 entries), per-warp slot bases into T, and the
+// FY thread -> leaf map; returns 1 if some bucket exceeds L (the item then
+// goes to the general kernel).
+template <int EB, bool NARROW>
+__device__ __forceinline__ uint32_t s_scan(const RunParams& rp, const XView<EB>& V, uint32_t* bst, uint16_t* perm,
+                                           uint64_t start, uint32_t m, uint32_t sid) {
+    const uint32_t k = rp.k;
     uint32_t* T = V.T();
-    uint32_t* bst = V.bst();
-    uint32_t* gb = V.gb();
-    uint32_t* gj = V.gj();
-    const uint32_t b0 = 2 * tid;  // thread tid owns buckets 2tid, 2tid+1 (k <= 1024 < 2 x 1024)
-    uint32_t c0 = 0, c1 = 0;
-    if (b0 < k) {
-#pragma unroll 8
-        for (uint32_t w = 0; w < XW; ++w) {
-            const uint32_t c = T[w * kw + tid];
-            c0 += c & 0xFFFFu;
-            c1 += c >> 16;
+    uint32_t mine = 0, big = 0;
+    uint32_t x0, x1;
+    if (NARROW) {  // u32 counters: thread owns buckets [x0, x1)
+        const uint32_t per = (k + XSN - 1) / XSN;
+        x0 = min(k, sid * per);
+        x1 = min(k, x0 + per);
+        for (uint32_t x = x0; x < x1; ++x) {
+            uint32_t c = 0;
+            for (uint32_t w = 0; w < XSW; ++w) c += T[w * k + x];
+            big |= c > rp.L;
+            mine += c;
         }
-        if (b0 + 1 >= k) c1 = 0;
+    } else {  // packed u16 counters: thread owns words [x0, x1)
+        const uint32_t kw = (k + 1) >> 1;
+        const uint32_t per = (kw + XSN - 1) / XSN;
+        x0 = min(kw, sid * per);
+        x1 = min(kw, x0 + per);
+        for (uint32_t x = x0; x < x1; ++x) {
+            uint32_t c0 = 0, c1 = 0;
+            for (uint32_t w = 0; w < XSW; ++w) {
+                const uint32_t c = T[w * kw + x];
+                c0 += c & 0xFFFFu;
+                c1 += c >> 16;
+            }
+            big |= (c0 > rp.L) | (c1 > rp.L);
+            mine += c0 + c1;
+        }
     }
     uint32_t total;
-    const uint32_t ex = block_exclusive_sum<XNT>(c0 + c1, V.wsum(), &total);
-    if (b0 < k) {
-        bst[b0] = ex;
-        if (b0 + 1 < k) bst[b0 + 1] = ex + c0;
-    }
-    if (tid == 0) bst[k] = ctl->cur.len;
-    // rows of each 32-leaf group (16 threads) = its longest leaf
-    uint32_t gm = c0 > c1 ? c0 : c1;
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-        const uint32_t t2 = __shfl_xor_sync(0xFFFFFFFFu, gm, o);
-        gm = gm > t2 ? gm : t2;
-    }
-    if ((tid & 15u) == 0 && (tid >> 4) < 33) ctl->gh[tid >> 4] = gm;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t ngr = (k + 31) >> 5;
-        const uint32_t h = lane < ngr ? ctl->gh[lane] : 0u;
-        const uint32_t hj = ((h + 7) >> 3) * 2;  // partner words: 2 per 8-step Philox group
-        const uint32_t incl = warp_inclusive_sum(h), inclj = warp_inclusive_sum(hj);
-        if (lane < ngr) {
-            gb[lane] = incl - h;
-            gj[lane] = inclj - hj;
+    uint32_t run = s_exclusive_sum(mine, V.wsum(), &total, sid);
+    if (NARROW) {
+        for (uint32_t x = x0; x < x1; ++x) {
+            bst[x] = run;
+            for (uint32_t w = 0; w < XSW; ++w) {
+                const uint32_t c = T[w * k + x];
+                T[w * k + x] = run;
+                run += c;
+            }
         }
-        const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, h);
-        if (lane == 31)
-            ctl->defer = (mx > rp.L || mx > 256u || incl * 32u > XCfg<EB>::COLCAP || inclj * 128u > V.Ly.jbbytes)
-                             ? 1u
-                             : 0u;
-    }
-    __syncthreads();
-    if (ctl->defer == 0) {
-        // per-warp row bases: T[w][b] = gb(b / 32) + sum_{w'<w} cnt[w'][b]
-        if (b0 < k) {
-            uint32_t r0 = gb[b0 >> 5], r1 = gb[(b0 + 1) >> 5];
-#pragma unroll 8
-            for (uint32_t w = 0; w < XW; ++w) {
-                const uint32_t c = T[w * kw + tid];
-                T[w * kw + tid] = (r0 & 0xFFFFu) | (r1 << 16);
+    } else {
+        const uint32_t kw = (k + 1) >> 1;
+        for (uint32_t x = x0; x < x1; ++x) {
+            uint32_t r0 = run, t0 = 0;
+            for (uint32_t w = 0; w < XSW; ++w) t0 += T[w * kw + x] & 0xFFFFu;
+            uint32_t r1 = run + t0;
+            bst[2 * x] = r0;
+            if (2 * x + 1 < k) bst[2 * x + 1] = r1;
+            for (uint32_t w = 0; w < XSW; ++w) {
+                const uint32_t c = T[w * kw + x];
+                T[w * kw + x] = (r0 & 0xFFFFu) | (r1 << 16);
                 r0 += c & 0xFFFFu;
                 r1 += c >> 16;
             }
+            run = r1;
         }
-    } else if (tid == 0) {
-        rp.flags[ctl->cur.child] = 1;  // hand the item to the general kernel
     }
+    if (sid == 0) bst[k] = m;
+    // any bucket > L anywhere in the group? (wsum[XSW] held the total: reused as the flag)
+    const bool anyw = __any_sync(0xFFFFFFFFu, big != 0);
+    uint32_t* cls = V.wsum();  // 32 class counters live past the XSW+1 scan words
+    if ((sid & 31u) == 0 && anyw) cls[XSW] = 0xFFFFFFFFu;
+    if (sid < 32) cls[XSW + 1 + sid] = 0;
+    bar_group(kBarS, XSN);
+    const uint32_t defer = cls[XSW] == 0xFFFFFFFFu ? 1u : 0u;
+    // FY thread -> leaf map: with u32 elements and k <= 256 (k % 32 == 0),
+    // leaves are dealt to the FY warps by the bank their Fisher-Yates steps
+    // start from, so a warp's lanes touch A[i] in (mostly) distinct banks;
+    // otherwise thread f takes leaf f.
+    const bool deal = EB == 4 && k <= XF && (k & 31u) == 0;  // positions p -> FY threads [0, k), bijective
+    uint32_t c = 0, rk = 0;
+    const uint32_t w0 = (uint32_t)((start * EB) & 15u) >> 2;  // word offset of element 0
+    if (deal && sid < k) {
+        // fy_leaf walks i = 8g + jj with the warp's lanes in lockstep over (group
+        // iteration n, jj), g = gt - n, gt = (cm - 1) >> 3: lane banks differ iff
+        // (start + 8 gt) mod 32 differ
+        const uint32_t s0 = bst[sid], cm = bst[sid + 1] - s0;
+        c = (w0 + s0 + 8u * ((cm ? cm - 1u : 0u) >> 3)) & 31u;
+        rk = atomicAdd(&cls[XSW + 1 + c], 1u);
+    }
+    bar_group(kBarS, XSN);
+    if (sid < 32) {
+        const uint32_t n = cls[XSW + 1 + sid];
+        const uint32_t incl = warp_inclusive_sum(n);
+        cls[XSW + 1 + sid] = incl - n;
+    }
+    bar_group(kBarS, XSN);
+    if (sid < k) {
+        if (deal) {
+            const uint32_t W = (k + 31) >> 5;  // FY warps in use
+            const uint32_t p = cls[XSW + 1 + c] + rk;  // position in bank order
+            // position p -> FY thread (warp p % W, lane p / W)
+            perm[(p % W) * 32u + p / W] = (uint16_t)sid;
+        } else {
+            perm[sid] = (uint16_t)sid;
+        }
+    }
+    bar_group(kBarS, XSN);
+    return defer;
 }
 
-// ---- phase 3: placement, contiguous buffer bi -> column layout in bc.
-template <int EB, bool NARROW>
-__device__ __forceinline__ void place_phase(const XView<EB>& V, uint32_t kw, uint32_t bi, uint32_t bc) {
+// Stable in-place scatter of the item inside its buffer: every S thread
+// holds its elements in registers across a group barrier, then each takes
+// its slot with one ordered shared atomic (warp rounds in position order).
+template <int EB, bool NARROW, bool ORD>
+__device__ __forceinline__ void s_place(const XView<EB>& V, const XItem& it, unsigned char* base, uint32_t w) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
-    XCtl* ctl = V.ctl();
-    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    const uint64_t start = ctl->cur.start;
-    const XRange<NARROW> xr(start - ctl->cur.origin, ctl->cur.len);
+    constexpr uint32_t R = XCfg<EB>::R;
+    const uint32_t lane = threadIdx.x & 31u, kw = NARROW ? V.k : (V.k + 1) >> 1;
+    const XRange<NARROW> xr(it.start - it.origin, it.len);
     const int32_t eb0 = (int32_t)(w * xr.qg * xr.dpg) - (int32_t)xr.doff;
     const uint32_t e_lo = eb0 > 0 ? (uint32_t)eb0 : 0u;
     const int32_t ehi = min((int32_t)((w + 1) * xr.qg * xr.dpg) - (int32_t)xr.doff, (int32_t)xr.m);
     const uint32_t len = ehi > (int32_t)e_lo ? (uint32_t)ehi - e_lo : 0u;
-    const E* in = reinterpret_cast<const E*>(item_base<EB>(V.buf(bi), start)) + e_lo;
+    E* el = reinterpret_cast<E*>(base);
     const D* dp = reinterpret_cast<const D*>(V.draws()) + xr.doff + e_lo;
-    E* col = reinterpret_cast<E*>(V.buf(bc));
     uint32_t* Tw = V.T() + w * kw;
-    // whole rounds of 32 in position order, then the partial last one
-    const uint32_t nfull = len & ~31u;
-#pragma unroll 4
-    for (uint32_t i0 = 0; i0 < nfull; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const uint32_t b = dp[i];
-        const E x = in[i];
-        const uint32_t shb = (b & 1u) << 4;
-        const uint32_t row = (atomicAdd(&Tw[b >> 1], 1u << shb) >> shb) & 0xFFFFu;
-        col[row * 32u + (b & 31u)] = x;
-    }
-    if (nfull < len) {
-        const uint32_t i = nfull + lane;
-        const bool valid = i < len;
-        const uint32_t ii = valid ? i : nfull;
-        const uint32_t b = valid ? (uint32_t)dp[ii] : 0u;
-        const E x = in[ii];
-        const uint32_t shb = (b & 1u) << 4;
-        const uint32_t row = (atomicAdd(&Tw[b >> 1], valid ? (1u << shb) : 0u) >> shb) & 0xFFFFu;
-        if (valid) col[row * 32u + (b & 31u)] = x;
-    }
-}
-
-// Exact Lemire16 decision for the steps flagged by the cheap pre-check
-// (low part < s), with the retry stream of D5 (out of line: rare).
-static __device__ __noinline__ void partner_fixup(uint32_t (&pk)[2], uint32_t rej, const uint32_t (&wv)[4],
-                                                  PhiloxKey key, uint64_t qq, uint32_t g, uint32_t mb) {
-    for (uint32_t jj = 0; jj < 8; ++jj) {
-        const uint32_t i = g * 8u + jj;
-        if (!((rej >> jj) & 1u) || i < 1 || i >= mb) continue;
-        const uint32_t vv = (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu;
-        const uint32_t j = fy16_from_lane(vv, key, qq, i);
-        pk[jj >> 2] = (pk[jj >> 2] & ~(0xFFu << ((jj & 3u) * 8u))) | ((j & 0xFFu) << ((jj & 3u) * 8u));
-    }
-}
-
-// ---- phase 4: partners j_i, i = 1 .. mb-1 of every leaf (D5: leaf id =
-// problem position of the leaf start, one Philox block per 8 steps,
-// Lemire16), packed 4 per word, in the leaves' column layout: word w (steps
-// 4w .. 4w+3) of leaf b at jb[32 (gj(b/32) + w) + (b & 31)].  Thread t takes
-// leaf t % k and every (1024/k)-th Philox group of it.
-template <int EB>
-__device__ __forceinline__ void partner_phase(const RunParams& rp, const XView<EB>& V) {
-    XCtl* ctl = V.ctl();
-    const uint32_t k = rp.k, tid = threadIdx.x;
-    const uint32_t* bst = V.bst();
-    const uint32_t* gj = V.gj();
-    const uint64_t P0 = ctl->cur.start - ctl->cur.origin;
-    const PhiloxKey key = make_key(ctl->cur.key);
-    const uint32_t per = XNT / k >= 2 ? XNT / k : 1;  // threads per leaf
-    if (per > 1 && tid >= per * k) return;
-    const uint32_t sub = per > 1 ? tid / k : 0;
-    const uint32_t bstep = per > 1 ? k : XNT;
-    for (uint32_t b = per > 1 ? tid % k : tid; b < k; b += bstep) {
-        const uint32_t s0 = bst[b], mb = bst[b + 1] - s0;
-        if (mb < 2) continue;
-        const uint64_t qq = P0 + s0;
-        uint32_t* jw = V.jb() + gj[b >> 5] * 32u + (b & 31u);
-        const uint32_t ngr = ((mb - 1) >> 3) + 1;
-        for (uint32_t g = sub; g < ngr; g += per) {
-            const uint4 w4 = fy16_group_words(key, qq, g);
-            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
-            uint32_t pk[2] = {0u, 0u};
-            uint32_t rej = 0;  // steps whose 16-bit lane Lemire may reject (rare)
+    E v[R];
+    const uint32_t ilast = len ? len - 1 : 0u;
 #pragma unroll
-            for (uint32_t jj = 0; jj < 8; ++jj) {
-                const uint32_t i = g * 8u + jj;
-                const uint32_t vv = (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu;
-                const uint32_t sb = i + 1, mm = vv * sb;
-                rej |= ((mm & 0xFFFFu) < sb ? 1u : 0u) << jj;
-                pk[jj >> 2] |= ((mm >> 16) & 0xFFu) << ((jj & 3u) * 8u);
-            }
-            if (__builtin_expect(rej != 0, 0)) partner_fixup(pk, rej, wv, key, qq, g, mb);
-            jw[(2 * g) * 32u] = pk[0];
-            jw[(2 * g + 1) * 32u] = pk[1];
-        }
+    for (uint32_t r = 0; r < R; ++r) {
+        const uint32_t i = r * 32u + lane;
+        v[r] = el[e_lo + (i < len ? i : ilast)];  // unconditional: keeps v[] in registers
     }
-}
-
-// ---- phase 5: Fisher-Yates of every leaf (threads 0..255), column layout in
-// bc -> final elements to the contiguous item layout in bi.
-template <int EB>
-__device__ __forceinline__ uint32_t fy_phase(const RunParams& rp, const XView<EB>& V, uint32_t bi, uint32_t bc) {
-    using E = typename ElemT<EB>::type;
-    const uint32_t tid = threadIdx.x, k = rp.k;
-    XCtl* ctl = V.ctl();
-    const uint32_t* bst = V.bst();
-    const uint32_t* gb = V.gb();
-    const uint32_t* gj = V.gj();
-    E* col0 = reinterpret_cast<E*>(V.buf(bc));
-    E* out0 = reinterpret_cast<E*>(item_base<EB>(V.buf(bi), ctl->cur.start));
-    uint32_t fyn = 0;
-    for (uint32_t b = tid; b < k; b += XFYT) {
-        const uint32_t s0 = bst[b], mb = bst[b + 1] - s0;
-        if (mb == 0) continue;
-        E* c = col0 + gb[b >> 5] * 32u + (b & 31u);  // leaf element t at c[32 t]
-        E* o = out0 + s0;
-        if (mb >= 2) {
-            fyn += mb;
-            // Fig. 1 for i = mb-1 .. 1: swap(A[i], A[j_i]).  Position i is final
-            // after step i: it goes to o[i], and A[i] is never read again.
-            // Software-pipelined: the loads of step i-1 are issued before the
-            // store of step i and patched when step i wrote the same place
-            // (j_i == i-1, or j_{i-1} == j_i).
-            const uint32_t* jw = V.jb() + gj[b >> 5] * 32u + (b & 31u);
-            uint32_t i = mb - 1;
-            uint32_t word = jw[(i >> 2) * 32u];
-            uint32_t jc = (word >> ((i & 3u) * 8u)) & 0xFFu;
-            E x = c[i * 32u], y = c[jc * 32u];
-            for (; i >= 2; --i) {
-                const uint32_t in = i - 1;
-                if ((in & 3u) == 3u) word = jw[(in >> 2) * 32u];
-                const uint32_t jn = (word >> ((in & 3u) * 8u)) & 0xFFu;
-                E xn = c[in * 32u];
-                E yn = c[jn * 32u];
-                c[jc * 32u] = x;
-                o[i] = y;
-                xn = (jc == in) ? x : xn;
-                yn = (jn == jc) ? x : yn;
-                x = xn;
-                y = yn;
-                jc = jn;
-            }
-            c[jc * 32u] = x;  // step 1
-            o[1] = y;
-        }
-        o[0] = c[0];
-    }
-    return fyn;
-}
-
-// ------------------------------------------------------------- loop ---
-template <int EB, bool NARROW>
-__device__ __forceinline__ void run(const RunParams& rp, const LevelParams& lp, const XView<EB>& V, uint32_t nchild) {
-    XCtl* ctl = V.ctl();
-    const uint32_t k = rp.k, kw = (k + 1) >> 1, tid = threadIdx.x;
-    const unsigned char* src = lp.dst;  // the level's output buffer holds the children
-    const uint32_t lvl = lp.level + 1;
-    // prologue: load + draws/counts of the first item, search of the second
-    if (ctl->cur.valid) {
-        if (tid == 0 || (tid >= 32 && tid < 40)) issue_load<EB>(V, ctl->cur, src, 0);
-        draw_count_phase<EB, NARROW>(rp, V, ctl->cur, lvl, 0, XW);
-    }
-    if (tid == 64) ctl->nxt = find_next<EB>(rp, lp, nchild, ctl->cursor);
-    __syncthreads();
-    for (uint32_t t = 0; ctl->cur.valid; ++t) {
-        const uint32_t bi = t & 1u, bc = bi ^ 1u;
-        const bool dbg = blockIdx.x == 0 && tid == 0 && ctl->dbg_it < 40;
-        if (dbg) rp.hdr->clk[ctl->dbg_it * 6 + 0] = clock64();
-        // 2. scan (the counts are in the tables); the load of this item and
-        //    the read-out of bc's previous contents complete
-        if (tid >= 32 && tid < 40) cp_async_wait_all();
-        scan_phase<EB>(rp, V);
-        if (tid == 0) bulk_wait_read0();
-        mbar_wait(&ctl->bar[bi], ctl->ph[bi]);
-        __syncthreads();
-        if (dbg) rp.hdr->clk[ctl->dbg_it * 6 + 1] = clock64();
-        const bool placed = ctl->defer == 0;
-        // 3. placement bi -> bc (column layout)
-        if (placed) place_phase<EB, NARROW>(V, kw, bi, bc);
-        __syncthreads();
-        if (dbg) rp.hdr->clk[ctl->dbg_it * 6 + 2] = clock64();
-        // 4. partners
-        if (placed) partner_phase<EB>(rp, V);
-        __syncthreads();
-        if (dbg) rp.hdr->clk[ctl->dbg_it * 6 + 3] = clock64();
-        // 5. Fisher-Yates bc -> bi (warps 0..7) | draws + counts of the next
-        //    item and the search of the one after it (warps 8..31)
-        if (tid < XFYT) {
-            if (placed) {
-                uint32_t fyn = fy_phase<EB>(rp, V, bi, bc);
-                for (int o = 16; o > 0; o >>= 1) fyn += __shfl_xor_sync(0xFFFFFFFFu, fyn, o);
-                if ((tid & 31u) == 0 && fyn) atomicAdd(&ctl->st_fy, (unsigned long long)fyn);
-            }
-            if (dbg) rp.hdr->clk[ctl->dbg_it * 6 + 4] = clock64();
+    bar_group(kBarS, XSN);
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) {
+        if (r * 32u >= len) break;  // warp-uniform
+        const uint32_t i = r * 32u + lane;
+        const bool valid = i < len;
+        const uint32_t b = valid ? (uint32_t)dp[i] : 0u;
+        uint32_t slot;
+        if (ORD && NARROW) {
+            slot = atomicAdd(&Tw[b], valid ? 1u : 0u);
+        } else if (ORD) {
+            const uint32_t shb = (b & 1u) << 4;
+            slot = (atomicAdd(&Tw[b >> 1], valid ? (1u << shb) : 0u) >> shb) & 0xFFFFu;
+        } else if (NARROW) {
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu);
+            slot = valid ? Tw[b] + __popc(peers & lanemask_lt()) : 0u;
+            __syncwarp();
+            if (valid && (peers & lanemask_lt()) == 0) Tw[b] += __popc(peers);
+            __syncwarp();
         } else {
-            const XItem nx = ctl->nxt;
-            if (nx.valid) draw_count_phase<EB, NARROW>(rp, V, nx, lvl, XFYT / 32, XW - XFYT / 32);
-            if (tid == XFYT) ctl->nxt2 = nx.valid ? find_next<EB>(rp, lp, nchild, ctl->cursor) : XItem{};
+            slot = warp_rank(Tw, b, valid, false);
         }
-        __syncthreads();
-        if (dbg) rp.hdr->clk[ctl->dbg_it * 6 + 5] = clock64();
-        // 6. store bi (aligned body: bulk async copy; head/tail words by threads
-        //    32..95), load the next item into bc (free again)
-        if (placed) {
-            const uint64_t x0 = ctl->cur.start * EB, x1 = (ctl->cur.start + ctl->cur.len) * EB;
-            const uint64_t fl = x0 & ~15ull;
-            const uint64_t A0 = (x0 + 15) & ~15ull, B0 = x1 & ~15ull;
-            const bool body = B0 > A0;
-            unsigned char* ob = V.buf(bi);
-            if (tid == 0 && body) {
-                fence_proxy_async();
-                bulk_s2g(rp.buf0 + A0, ob + (A0 - fl), (uint32_t)(B0 - A0));
-                bulk_commit();
-            }
-            const uint64_t hEnd = body ? A0 : x1;
-            const uint32_t nh = (uint32_t)((hEnd - x0) >> 2);
-            const uint64_t tBeg = body ? B0 : x1;
-            const uint32_t nt = (uint32_t)((x1 - tBeg) >> 2);
-            if (tid >= 32 && tid - 32 < nh)
-                *reinterpret_cast<uint32_t*>(rp.buf0 + x0 + 4 * (tid - 32)) =
-                    *reinterpret_cast<const uint32_t*>(ob + (x0 - fl) + 4 * (tid - 32));
-            else if (tid >= 64 && tid - 64 < nt)
-                *reinterpret_cast<uint32_t*>(rp.buf0 + tBeg + 4 * (tid - 64)) =
-                    *reinterpret_cast<const uint32_t*>(ob + (tBeg - fl) + 4 * (tid - 64));
-        }
-        __syncthreads();  // head/tail words of the store are out
-        const XItem nx = ctl->nxt;
-        if (nx.valid && (tid == 0 || (tid >= 32 && tid < 40))) issue_load<EB>(V, nx, src, bc);
-        if (tid == 0) {
-            ctl->dbg_it++;
-            ctl->ph[bi] ^= 1u;
-            if (placed) ctl->st_fin += ctl->cur.len;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            ctl->cur = ctl->nxt;
-            ctl->nxt = ctl->nxt2;
-            ctl->defer = 0;
-        }
-        __syncthreads();
+        if (valid) el[slot] = v[r];
     }
-    if (tid == 0) bulk_wait0();
 }
 
-template <int EB, bool NARROW>
+// ------------------------------------------------------------- kernel ---
+template <int EB, bool NARROW, bool ORD>
 __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParams lp) {
     const XView<EB> V(rp.k);
     XCtl* ctl = V.ctl();
+    const uint32_t tid = threadIdx.x, k = rp.k;
     const uint32_t nchild = lp.ctr->nseg * rp.k;
-    if (threadIdx.x == 0) {
+    const uint32_t lvl = lp.level + 1;
+    if (tid == 0) {
         ctl->cursor = blockIdx.x;
-        ctl->defer = 0;
-        ctl->ph[0] = ctl->ph[1] = 0;
-        ctl->dbg_it = 0;
-        ctl->st_fin = 0;
-        ctl->st_fy = 0;
-        mbar_init(&ctl->bar[0], 1);
-        mbar_init(&ctl->bar[1], 1);
+        ctl->dbg_s = ctl->dbg_f = 0;
+        ctl->st_fin = ctl->st_fy = 0;
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&ctl->full[i], 1);
+            mbar_init(&ctl->ready[i], 1);
+            mbar_init(&ctl->fydone[i], 1);
+            ctl->defer[i] = 0;
+        }
         fence_mbar_init();
-        ctl->cur = find_next<EB>(rp, lp, nchild, ctl->cursor);
-        ctl->nxt.valid = 0;
-        ctl->nxt2.valid = 0;
     }
     __syncthreads();
-    run<EB, NARROW>(rp, lp, V, nchild);
+    const bool dbgcta = (rp.dbg & 4u) && blockIdx.x == 0;
+    if (tid >= XC && tid < XS0) {
+        // ---------------- C: loads and stores
+        c_load_next<EB>(rp, lp, V, nchild, 0);
+        c_load_next<EB>(rp, lp, V, nchild, 1);
+        uint32_t ph[2] = {0, 0};
+        for (uint32_t t = 0;; ++t) {
+            const uint32_t bi = t & 1u;
+            mbar_wait(&ctl->fydone[bi], ph[bi]);
+            ph[bi] ^= 1u;
+            const XItem it = ctl->item[bi];
+            if (!it.valid) break;
+            if (!ctl->defer[bi]) {
+                c_store<EB>(rp, V, it, bi);
+                if (tid == XC) ctl->st_fin += it.len;
+            }
+            __syncwarp();
+            c_load_next<EB>(rp, lp, V, nchild, bi);
+        }
+        if (tid == XC) bulk_wait0();
+    } else if (tid >= XS0) {
+        // ---------------- S: draws, counts, scan, in-place stable scatter
+        const uint32_t sid = tid - XS0, w = sid >> 5;
+        uint32_t ph[2] = {0, 0};
+        for (uint32_t t = 0;; ++t) {
+            const uint32_t bi = t & 1u;
+            // the descriptor is written before the load is issued: wait for
+            // the load (mbarrier acquire), then read it
+            mbar_wait(&ctl->full[bi], ph[bi]);
+            ph[bi] ^= 1u;
+            const XItem it = ctl->item[bi];
+            const bool dbg = dbgcta && sid == 0 && ctl->dbg_s < 40;
+            if (dbg) rp.hdr->clk[ctl->dbg_s * 6 + 0] = clock64();
+            uint32_t defer = 1;
+            if (it.valid && (rp.dbg & 16u)) {  // timing experiment: S does no work (F runs alone)
+                if (sid < k) V.perm(bi)[sid] = (uint16_t)sid;
+                for (uint32_t b = sid; b <= k; b += XSN) V.bst(bi)[b] = (uint32_t)((uint64_t)b * it.len / k);
+                defer = 0;
+            } else if (it.valid) {
+                s_count<EB, NARROW>(rp, V, it, lvl, w);
+                bar_group(kBarS, XSN);
+                defer = s_scan<EB, NARROW>(rp, V, V.bst(bi), V.perm(bi), it.start, it.len, sid);
+                if (dbg) rp.hdr->clk[ctl->dbg_s * 6 + 1] = clock64();
+                if (!defer) s_place<EB, NARROW, ORD>(V, it, item_base<EB>(V.buf(bi), it.start), w);
+                else if (sid == 0) rp.flags[it.child] = 1;  // the general kernel takes it
+            }
+            bar_group(kBarS, XSN);
+            if (sid == 0) {
+                ctl->defer[bi] = defer;
+                if (dbg) rp.hdr->clk[ctl->dbg_s++ * 6 + 2] = clock64();
+                mbar_arrive1(&ctl->ready[bi]);
+            }
+            if (!it.valid) break;
+        }
+    } else {
+        // ---------------- F: Fisher-Yates of every leaf of item t
+        uint32_t ph[2] = {0, 0};
+        unsigned long long fyn = 0;
+        for (uint32_t t = 0;; ++t) {
+            const uint32_t bi = t & 1u;
+            mbar_wait(&ctl->ready[bi], ph[bi]);
+            ph[bi] ^= 1u;
+            const XItem it = ctl->item[bi];
+            const bool dbg = dbgcta && tid == 0 && ctl->dbg_f < 40;
+            if (dbg) rp.hdr->clk[ctl->dbg_f * 6 + 3] = clock64();
+            if (it.valid && !ctl->defer[bi] && !(rp.dbg & 8u)) {  // dbg 8: timing experiment, no FY
+                const uint32_t* bst = V.bst(bi);
+                unsigned char* base = item_base<EB>(V.buf(bi), it.start);
+                const uint64_t P0 = it.start - it.origin;
+                const PhiloxKey key = make_key(it.key);
+                const uint16_t* perm = V.perm(bi);
+                for (uint32_t f = tid; f < k; f += XF) {
+                    const uint32_t b = (k <= XF) ? perm[f] : f;
+                    const uint32_t s0 = bst[b], cm = bst[b + 1] - s0;
+                    if (cm >= 2) {
+                        fy_leaf<EB>(base, s0, cm, P0 + s0, key);
+                        fyn += cm;
+                    }
+                }
+            }
+            bar_group(kBarF, XF);
+            if (tid == 0) {
+                if (dbg) rp.hdr->clk[ctl->dbg_f++ * 6 + 4] = clock64();
+                mbar_arrive1(&ctl->fydone[bi]);
+            }
+            if (!it.valid) break;
+        }
+        for (int o = 16; o > 0; o >>= 1) fyn += __shfl_xor_sync(0xFFFFFFFFu, fyn, o);
+        if ((tid & 31u) == 0 && fyn) atomicAdd(&ctl->st_fy, fyn);
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t lvl = lp.level + 1;
+    if (tid == 0) {
         atomicAdd((unsigned long long*)&rp.hdr->finished, ctl->st_fin);
         atomicAdd((unsigned long long*)&rp.hdr->scattered_smem[lvl < kMaxLevels ? lvl : 0], ctl->st_fin);
         atomicAdd((unsigned long long*)&rp.hdr->fy_elems, ctl->st_fy);
@@ -631,32 +615,35 @@ __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParam
 }
 
 template <int EB>
-static void* fast_fn(bool narrow) {
-    return narrow ? (void*)k_finish_fast<EB, true> : (void*)k_finish_fast<EB, false>;
+static void* fast_fn(bool narrow, bool ord) {
+    if (ord) return narrow ? (void*)k_finish_fast<EB, true, true> : (void*)k_finish_fast<EB, false, true>;
+    return narrow ? (void*)k_finish_fast<EB, true, false> : (void*)k_finish_fast<EB, false, false>;
 }
-static void* fast_kernel(uint32_t eb, bool narrow) {
+static void* fast_kernel(uint32_t eb, bool narrow, bool ord) {
     switch (eb) {
-    case 4: return fast_fn<4>(narrow);
-    case 8: return fast_fn<8>(narrow);
-    default: return fast_fn<16>(narrow);
+    case 4: return fast_fn<4>(narrow, ord);
+    case 8: return fast_fn<8>(narrow, ord);
+    default: return fast_fn<16>(narrow, ord);
     }
 }
 
 cudaError_t configure_fast(uint32_t eb, uint32_t k) {
     const uint32_t smem = fast_smem_bytes(eb, k);
     if (smem > kSmemLimit) return cudaErrorInvalidValue;
-    for (int nr = 0; nr < 2; ++nr) {
-        cudaError_t e = cudaFuncSetAttribute(fast_kernel(eb, nr != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem);
-        if (e) return e;
-    }
+    for (int nr = 0; nr < 2; ++nr)
+        for (int o = 0; o < 2; ++o) {
+            cudaError_t e = cudaFuncSetAttribute(fast_kernel(eb, nr != 0, o != 0),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e) return e;
+        }
     return cudaSuccess;
 }
 
 cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     const uint32_t smem = fast_smem_bytes(rp.eb, rp.k);
     void* args[] = {(void*)&rp, (void*)&lp};
-    return cudaLaunchKernel(fast_kernel(rp.eb, rp.bp.narrow != 0), dim3(grid), dim3(XNT), args, smem, s);
+    return cudaLaunchKernel(fast_kernel(rp.eb, rp.bp.narrow != 0, rp.rank_ordered != 0), dim3(grid), dim3(XNT), args,
+                            smem, s);
 }
 
 }  // namespace shuf

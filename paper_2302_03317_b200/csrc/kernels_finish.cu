@@ -52,6 +52,7 @@ struct FinCtl {
     uint64_t seg_start, seg_origin, seg_key;
     uint64_t ub[kUnit + 1];  // unit child boundaries (relative to seg_start)
     uint64_t rec;            // item record index (defer mode)
+    uint32_t dbg_it;         // items processed by CTA 0 (phase clocks, SHUF_DBG=2)
     unsigned long long st_finished, st_smem[32];
 };
 
@@ -291,10 +292,14 @@ __device__ __forceinline__ void process_item(const RunParams& rp, const Fin& F, 
     const bool leaf = m <= rp.L;
     FinCtl* ctl = F.ctl();
     if (tid == 0) ctl->st_finished += m;
+    const bool dbg = (rp.dbg & 2u) && blockIdx.x == 0 && tid == 0 && ctl->dbg_it < 40;
+    long long* clk = rp.hdr->clk + (dbg ? ctl->dbg_it * 6 : 0);
+    if (dbg) clk[0] = clock64();
     if (!leaf && it.level < rp.max_levels) {
         // OUT was last read by the previous item's bulk store
         if (tid == 0) bulk_wait_read0();
         smem_level<EB, NARROW, ORD>(rp, F, in, out, 0, m, P0, it.level, key, true);
+        if (dbg) clk[1] = clock64();
         const bool big = any_big_child(rp, F);
         const bool deep = big && it.level + 1 < rp.max_levels;
         if (!deep && next) item_load<EB>(*next, src, F.in(), F.bar());  // IN is free: overlap the next load
@@ -313,9 +318,11 @@ __device__ __forceinline__ void process_item(const RunParams& rp, const Fin& F, 
             }
             for (uint32_t b = tid; b <= rp.k; b += NTF) reinterpret_cast<uint16_t*>(r + 24)[b] = (uint16_t)F.bst()[b];
         } else {
+            if (dbg) clk[2] = clock64();
             handle_children<EB>(rp, F, out, 0, m, P0, it.level, key, F.front(0), fy_local);
         }
         __syncthreads();
+        if (dbg) clk[3] = clock64();
         uint32_t nf = ctl->nfront, cur = 0, lv = it.level + 1;
         __syncthreads();
         while (nf > 0) {  // deeper in-smem levels (rare when S_fuse / k << L): OUT -> IN -> OUT
@@ -339,6 +346,10 @@ __device__ __forceinline__ void process_item(const RunParams& rp, const Fin& F, 
         if (deep && next) item_load<EB>(*next, src, F.in(), F.bar());
         __syncthreads();
         item_store<EB>(it, rp.buf0, F.out());
+        if (dbg) {
+            clk[4] = clock64();
+            ctl->dbg_it++;
+        }
     } else {
         // leaf-only (or level-limited) item: in place in IN
         const bool fy = leaf && rp.run_leaves && m >= 2;
@@ -367,6 +378,7 @@ __device__ __forceinline__ void fin_init(const Fin& F) {
         fence_mbar_init();
         FinCtl* c = F.ctl();
         c->phase = 0;
+        c->dbg_it = 0;
         c->st_finished = 0;
         for (int i = 0; i < 32; ++i) c->st_smem[i] = 0;
     }

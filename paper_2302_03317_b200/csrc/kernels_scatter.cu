@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
     s_issue_load<EB>(cur.q0, cnt, src, sm + Ly.buf0, &bar[0]);
     unsigned long long scattered = cur.q1 - cur.q0;
     bool new_chunk = true;
-    const bool dbgc = blockIdx.x == 0 && tid == 0 && lp.level == 0;
+    const bool dbgc = (rp.dbg & 1u) && blockIdx.x == 0 && tid == 0 && lp.level == 0;
     for (uint32_t it = 0; cur.chunk < nchunk; ++it) {
         const bool dbg = dbgc && it < 40;
         if (dbg) rp.hdr->sclk[it * 6 + 0] = clock64();

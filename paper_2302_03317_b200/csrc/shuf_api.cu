@@ -269,11 +269,11 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     p->scatter_smem = scatter_smem_bytes(p->eb, p->k);
     if ((e = configure_finish(p->finish_smem))) return e;
     if ((e = configure_scatter(p->scatter_smem))) return e;
-    // fast finish (kernels_fast.cu, experimental): ordered-atomic ranking only;
-    // SHUF_FAST_FINISH=1 enables it
+    // pipelined finish (kernels_fast.cu) for single-level items; SHUF_FAST_FINISH=0
+    // leaves every item to the general finish kernel
     {
         const char* ff = std::getenv("SHUF_FAST_FINISH");
-        p->fast = (p->rank_ordered && p->k <= kMaxK && (ff && ff[0] == '1') &&
+        p->fast = (p->k <= kMaxK && !(ff && ff[0] == '0') &&
                    fast_smem_bytes(p->eb, p->k) <= kSmemLimit)
                       ? 1
                       : 0;

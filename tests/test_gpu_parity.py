@@ -156,15 +156,16 @@ _ENV_CASES = (
     "print('ok')\n")
 
 
-@pytest.mark.parametrize("env", [{"SHUF_FAST_FINISH": "1"}, {"SHUF_LEAF": "0"}, {"SHUF_DEFER": "1"},
-                                 {"SHUF_DEFER": "1", "SHUF_RANK_MODE": "match"}],
-                         ids=["fast_finish", "no_leaf_kernel", "deferred_leaves", "deferred_leaves_match"])
+@pytest.mark.parametrize("env", [{"SHUF_FAST_FINISH": "0"}, {"SHUF_FAST_FINISH": "0", "SHUF_RANK_MODE": "match"},
+                                 {"SHUF_LEAF": "0"}, {"SHUF_DEFER": "1", "SHUF_FAST_FINISH": "0"},
+                                 {"SHUF_DEFER": "1", "SHUF_FAST_FINISH": "0", "SHUF_RANK_MODE": "match"}],
+                         ids=["general_finish", "general_finish_match", "no_leaf_kernel", "deferred_leaves",
+                              "deferred_leaves_match"])
 def test_alternate_routes_bit_exact(env):
-    """Routes chosen per process by environment (kernels_fast.cu's warp-
-    specialised finish; leaves in the finish kernel instead of the leaf
-    kernel; leaves of fused items deferred to the leaf kernel) must give the
-    same bits as the oracle on every shape, handing whatever they do not take
-    to the general kernels."""
+    """Routes chosen per process by environment (the general finish kernel
+    instead of kernels_fast.cu's pipelined one; leaves in the finish kernel
+    instead of the leaf kernel; leaves of fused items deferred to the leaf
+    kernel) must give the same bits as the oracle on every shape."""
     import os
     import subprocess
     import sys

@@ -69,6 +69,25 @@ if "--scatter" in sys.argv:
         nx = c[256 + (it + 1) * 6]
         print(f"  tile {it}: {t[1]-t[0]:6d} {t[2]-t[1]:6d} {t[3]-t[2]:6d} {t[4]-t[3]:6d} {t[5]-t[4]:6d}  total {nx - t[0] if nx else 0:6d}")
     sys.exit(0)
+if os.environ.get("SHUF_DBG") == "4":
+    print("pipelined finish CTA 0 per item (cycles): S count+scan, S place, S period; F FY, F period")
+    for it in range(1, 30):
+        t = c[it * 6: it * 6 + 5]
+        if t[0] == 0:
+            break
+        n = c[(it + 1) * 6: (it + 1) * 6 + 5]
+        print(f"  item {it}: S {t[1]-t[0]:6d} {t[2]-t[1]:6d} per {n[0]-t[0] if n[0] else 0:6d} | "
+              f"F {t[4]-t[3]:6d} per {n[3]-t[3] if n[3] else 0:6d}")
+    sys.exit(0)
+if os.environ.get("SHUF_DBG") == "2":
+    print("general finish CTA 0 per item (cycles): smem level, any_big+next load, FY(handle_children)+sync, store issue, total")
+    for it in range(1, 30):
+        t = c[it * 6: it * 6 + 5]
+        if t[0] == 0:
+            break
+        nxt = c[(it + 1) * 6]
+        print(f"  item {it}: {t[1]-t[0]:6d} {t[2]-t[1]:6d} {t[3]-t[2]:6d} {t[4]-t[3]:6d}  total {nxt - t[0] if nxt else 0:6d}")
+    sys.exit(0)
 print("fast-finish CTA 0 per item (cycles): scan+wait, place, partners, FY, FY||draws+count(next), store+rotate, total")
 for it in range(1, 12):
     t = c[it * 6: it * 6 + 6]
