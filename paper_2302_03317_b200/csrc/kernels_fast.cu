@@ -146,44 +146,6 @@ __device__ __forceinline__ void child_of(const LevelParams& lp, uint32_t k, uint
     len = s1 - s0;
 }
 
-// Next child of this CTA's stride sequence that the fast path takes; flags
-// every child of at most S_fuse elements on the way (1: general kernel).
-template <int EB>
-__device__ __forceinline__ XItem find_next(const RunParams& rp, const LevelParams& lp, uint32_t nchild,
-                                           uint32_t& cursor) {
-    XItem it;
-    it.valid = 0;
-    const uint32_t lvl = lp.level + 1;
-    for (uint32_t c = cursor; c < nchild; c += gridDim.x) {
-        uint64_t start, len;
-        SegDesc sg;
-        child_of(lp, rp.k, c, start, len, sg);
-        if (len == 0 || len > rp.S_fuse) continue;  // empty, or an HBM segment of the next level
-        const bool leaf = len <= rp.L;
-        if (leaf && rp.leafk) continue;             // the leaf kernel's
-        const bool permutes = (!leaf && lvl < rp.max_levels) || (leaf && rp.run_leaves && len >= 2);
-        if (!permutes) {  // nothing to do unless it must be copied to ptr
-            rp.flags[c] = (lp.dst == rp.buf0) ? 0 : 1;
-            continue;
-        }
-        if (leaf || len > XCfg<EB>::SMAX || lvl + 1 > rp.max_levels || !rp.run_leaves) {
-            rp.flags[c] = 1;
-            continue;
-        }
-        rp.flags[c] = 0;
-        it.start = start;
-        it.origin = sg.origin;
-        it.key = sg.key;
-        it.len = (uint32_t)len;
-        it.child = c;
-        it.valid = 1;
-        cursor = c + gridDim.x;
-        return it;
-    }
-    cursor = 0xFFFFFFFFu;
-    return it;
-}
-
 template <int EB>
 struct XView {
     XLayout Ly;
@@ -237,13 +199,70 @@ __device__ __forceinline__ void c_store(const RunParams& rp, const XView<EB>& V,
     __syncwarp();
 }
 
+// find_next with the 32 lanes of warp C examining 32 children of the CTA's
+// stride sequence at once (the first taker wins; children before it are
+// flagged, the ones after it are examined again next time).
+template <int EB>
+__device__ __forceinline__ void find_next_warp(const RunParams& rp, const LevelParams& lp, uint32_t nchild,
+                                               XCtl* ctl, uint32_t bi) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lvl = lp.level + 1;
+    uint32_t cursor = ctl->cursor;
+    for (;;) {
+        if (cursor >= nchild) break;
+        const uint64_t c64 = (uint64_t)cursor + (uint64_t)lane * gridDim.x;
+        // with the fused list (k_plan) the stride sequence runs over its entries
+        const uint32_t c = (rp.max_fused && c64 < nchild) ? rp.fused[c64] : (uint32_t)c64;
+        bool take = false;
+        int flag = -1;  // -1: leave the flag alone, 0 / 1: write it
+        uint64_t start = 0, len = 0;
+        SegDesc sg;
+        if (c64 < nchild) {
+            child_of(lp, rp.k, c, start, len, sg);
+            const bool leaf = len <= rp.L;
+            if (len == 0 || len > rp.S_fuse || (leaf && rp.leafk)) {
+                // empty, an HBM segment of the next level, or the leaf kernel's
+            } else {
+                const bool permutes = (!leaf && lvl < rp.max_levels) || (leaf && rp.run_leaves && len >= 2);
+                if (!permutes) flag = (lp.dst == rp.buf0) ? 0 : 1;
+                else if (leaf || len > XCfg<EB>::SMAX || lvl + 1 > rp.max_levels || !rp.run_leaves) flag = 1;
+                else take = true;
+            }
+        }
+        const uint32_t tk = __ballot_sync(0xFFFFFFFFu, take);
+        const uint32_t first = tk ? (uint32_t)(__ffs(tk) - 1) : 32u;
+        if (lane < first && flag >= 0) rp.flags[c] = (unsigned char)flag;
+        if (tk) {
+            if (lane == first) {
+                rp.flags[c] = 0;
+                XItem& it = ctl->item[bi];
+                it.start = start;
+                it.origin = sg.origin;
+                it.key = sg.key;
+                it.len = (uint32_t)len;
+                it.child = c;
+                it.valid = 1;
+                ctl->cursor = (uint32_t)c64 + gridDim.x;
+            }
+            __syncwarp();
+            return;
+        }
+        cursor += 32u * gridDim.x;
+    }
+    if (lane == 0) {
+        ctl->item[bi].valid = 0;
+        ctl->cursor = 0xFFFFFFFFu;
+    }
+    __syncwarp();
+}
+
 // Find the next item, record it for buffer bi and start its load (warp C).
 template <int EB>
 __device__ __forceinline__ void c_load_next(const RunParams& rp, const LevelParams& lp, const XView<EB>& V,
                                             uint32_t nchild, uint32_t bi) {
     const uint32_t lane = threadIdx.x & 31u;
     XCtl* ctl = V.ctl();
-    if (lane == 0) ctl->item[bi] = find_next<EB>(rp, lp, nchild, ctl->cursor);
+    find_next_warp<EB>(rp, lp, nchild, ctl, bi);
     __syncwarp();
     const XItem it = ctl->item[bi];
     unsigned char* buf = V.buf(bi);
@@ -501,7 +520,7 @@ __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParam
     const XView<EB> V(rp.k);
     XCtl* ctl = V.ctl();
     const uint32_t tid = threadIdx.x, k = rp.k;
-    const uint32_t nchild = lp.ctr->nseg * rp.k;
+    const uint32_t nchild = rp.max_fused ? lp.ctr->nfuse : lp.ctr->nseg * rp.k;
     const uint32_t lvl = lp.level + 1;
     if (tid == 0) {
         ctl->cursor = blockIdx.x;

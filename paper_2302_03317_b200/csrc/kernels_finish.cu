@@ -477,8 +477,55 @@ struct ChildIter {
     }
 };
 
+// The level's fused list (k_plan): child indices c = s*k + b with
+// L < len <= S_fuse (the leaf kernel takes the shorter ones).
+struct ListIter {
+    const RunParams* rp;
+    const LevelParams* lp;
+    __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {  // warp 0, all lanes
+        const uint32_t lane = threadIdx.x & 31u;
+        if (lane == 0) {
+            ctl->have[slot] = 0;
+            const uint32_t k = rp->k;
+            while (ctl->u < ctl->units) {
+                const uint32_t c = rp->fused[ctl->u];
+                ctl->u += gridDim.x;
+                if (rp->fast && rp->flags[c] == 0) continue;  // taken by k_finish_fast
+                const SegDesc sg = lp->segs[c / k];
+                const uint32_t b = c % k;
+                const uint64_t base0 = lp->prefix[sg.cbase];
+                const uint64_t s0 = lp->prefix[sg.cbase + (uint64_t)b * sg.nchunks] - base0;
+                const uint64_t s1 = (b + 1 < k) ? lp->prefix[sg.cbase + (uint64_t)(b + 1) * sg.nchunks] - base0 : sg.len;
+                Item& it = ctl->items[slot];
+                it.start = sg.start + s0;
+                it.len = (uint32_t)(s1 - s0);
+                it.level = lp->level + 1;
+                it.origin = sg.origin;
+                it.key = sg.key;
+                ctl->have[slot] = 1;
+                break;
+            }
+        }
+        __syncwarp();
+    }
+};
+
 template <int EB, bool NARROW, bool ORD>
 __global__ void __launch_bounds__(NTF, 1) k_finish_children(RunParams rp, LevelParams lp) {
+    if (rp.max_fused) {  // iterate the fused list
+        const uint64_t units = lp.ctr->nfuse;
+        if (blockIdx.x >= units) return;
+        const Fin F(rp);
+        fin_init(F);
+        if (threadIdx.x == 0) {
+            F.ctl()->u = blockIdx.x;
+            F.ctl()->units = units;
+        }
+        __syncthreads();
+        ListIter iter{&rp, &lp};
+        run_items<EB, NARROW, ORD>(rp, F, iter, lp.dst);
+        return;
+    }
     const uint32_t groups = (rp.k + kUnit - 1) / kUnit;
     const uint64_t units = (uint64_t)lp.ctr->nseg * groups;
     if (blockIdx.x >= units) return;

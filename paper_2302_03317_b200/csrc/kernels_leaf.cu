@@ -25,10 +25,68 @@ extern __shared__ __align__(16) unsigned char lsm[];
 constexpr uint32_t kLeafThreads = 128;  // 4 warps per CTA
 constexpr uint32_t kLeafWarps = kLeafThreads / 32;
 
-// Slot bytes per warp: at least 16 KiB, and room for one leaf of L elements.
+// Slot bytes per warp: at least 16 KiB, and room for one leaf of L elements
+// plus its u16 Fisher-Yates partners (the warp-cooperative path).
 __host__ __device__ inline uint32_t leaf_slot_bytes(uint32_t eb, uint32_t L) {
-    uint32_t s = (L * eb + 32 + 15) & ~15u;
+    uint32_t s = ((L * eb + 32 + 15) & ~15u) + ((2 * L + 15) & ~15u) + ((L + 15) & ~15u);
     return s < 16384u ? 16384u : s;
+}
+
+// Fisher-Yates (Fig. 1) of ONE long leaf A[0..m) by a whole warp, bit for bit
+// the sequential result: the partners j_i (D5) are precomputed into P; then
+// in rounds the lanes take steps i = top, top-1, .., top-31 and the longest
+// prefix of them that touches pairwise distinct positions runs at once --
+// lane l conflicts if another lane shares its partner (every lane writes its
+// id to M[j], then reads it back: a different id means a shared partner;
+// flagging both lanes of a pair is conservative, hence still exact) or if an
+// earlier lane's partner is l's own position i_l (an earlier lane's i can
+// never be l's partner, as j_l <= i_l).
+template <int EB>
+__device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, unsigned char* M, uint32_t m, uint64_t q,
+                                             PhiloxKey key) {
+    using E = typename ElemT<EB>::type;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (m < 2) return;
+    const uint32_t ng = ((m - 1) >> 3) + 1;
+    for (uint32_t g = lane; g < ng; g += 32) {
+        const uint4 w = fy16_group_words(key, q, g);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (uint32_t jj = 0; jj < 8; ++jj) {
+            const uint32_t i = g * 8u + jj;
+            if (i >= 1 && i < m) {
+                const uint32_t v = (wv[jj >> 1] >> ((jj & 1u) * 16u)) & 0xFFFFu;
+                const uint32_t sb = i + 1, mm = v * sb;
+                uint32_t j = mm >> 16;
+                if (__builtin_expect((mm & 0xFFFFu) < sb, 0)) j = fy16_from_lane(v, key, q, i);
+                P[i] = (uint16_t)j;
+            }
+        }
+    }
+    __syncwarp();
+    E* A = reinterpret_cast<E*>(el);
+    int32_t top = (int32_t)m - 1;
+    while (top >= 1) {
+        const int32_t i = top - (int32_t)lane;
+        const bool valid = i >= 1;
+        const uint32_t j = valid ? (uint32_t)P[i] : 0u;
+        if (valid) M[j] = (unsigned char)lane;
+        __syncwarp();
+        const bool shared = valid && M[j] != lane;
+        const int32_t d = top - (int32_t)j;  // the lane whose position is my partner
+        const uint32_t hb = (valid && d < 32 && d > (int32_t)lane) ? (1u << d) : 0u;
+        const uint32_t hits = __reduce_or_sync(0xFFFFFFFFu, hb);
+        const bool conflict = valid && (shared || ((hits >> lane) & 1u));
+        const uint32_t cmask = __ballot_sync(0xFFFFFFFFu, conflict);
+        const uint32_t c = cmask ? (uint32_t)(__ffs(cmask) - 1) : min(32u, (uint32_t)top);
+        if (lane < c) {
+            const E a = A[i], b = A[j];
+            A[i] = b;
+            A[j] = a;
+        }
+        __syncwarp();
+        top -= (int32_t)c;
+    }
 }
 uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L) { return kLeafWarps * (leaf_slot_bytes(eb, L) + 16); }
 
@@ -145,23 +203,30 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
         const bool fy = len >= 2 && len <= rp.L && rp.run_leaves;
         const bool mine = len >= 1 && len <= rp.L && (fy || copy_out);
         if (mine) fin += len;
-        // ---- batches: leaves in lane order, packed into the slot
-        uint32_t todo = __ballot_sync(0xFFFFFFFFu, mine);
+        // long leaves (fewer than 8 fit the slot) run one at a time with the
+        // whole warp (fy_leaf_warp); the others one thread per leaf
         const uint32_t need = mine ? (((uint32_t)len * EB + 32 + 15) & ~15u) : 0u;
-        while (todo) {
-            // the batch: the longest run of pending lanes (in lane order) that fits
-            const uint32_t first = __ffs(todo) - 1;
+        const bool big = fy && need * 8u > slot_bytes;
+        uint32_t todo = __ballot_sync(0xFFFFFFFFu, mine && !big);
+        uint32_t todo_big = __ballot_sync(0xFFFFFFFFu, big);
+        while (todo | todo_big) {
             uint32_t off = 0;  // my slot offset if I am in the batch
             bool inb = false;
-            {
+            const bool coop = todo == 0;  // this batch: one long leaf, the whole warp
+            if (!coop) {
+                // the batch: the longest run of pending short leaves (in lane order) that fits
+                const uint32_t first = __ffs(todo) - 1;
                 const uint32_t pend = (todo >> lane) & 1u;
                 const uint32_t v = pend && lane >= first ? need : 0u;
                 const uint32_t incl = warp_inclusive_sum(v);
                 inb = pend && lane >= first && incl <= slot_bytes;
                 off = incl - v;
+                todo &= ~__ballot_sync(0xFFFFFFFFu, inb);
+            } else {
+                const uint32_t L0 = __ffs(todo_big) - 1;
+                inb = lane == L0;
+                todo_big &= ~(1u << L0);
             }
-            const uint32_t batch = __ballot_sync(0xFFFFFFFFu, inb);
-            todo &= ~batch;
             // ---- load: aligned body by one bulk copy per leaf, ends by 4-byte copies
             uint64_t x0 = 0, x1 = 0, A = 0, B = 0;
             uint32_t body = 0;
@@ -197,7 +262,17 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
             mbar_wait(bar, phase);
             phase ^= 1u;
             // ---- Fisher-Yates of my leaf (D5 draws keyed by the leaf start)
-            if (inb && fy) {
+            if (coop) {
+                const uint32_t L0 = __ffs(__ballot_sync(0xFFFFFFFFu, inb)) - 1;
+                const uint32_t m = (uint32_t)__shfl_sync(0xFFFFFFFFu, len, L0);
+                const uint64_t q = __shfl_sync(0xFFFFFFFFu, start - origin, L0);
+                const uint64_t K = __shfl_sync(0xFFFFFFFFu, key, L0);
+                const uint32_t a0 = __shfl_sync(0xFFFFFFFFu, (uint32_t)(x0 & 15u), L0);
+                uint16_t* P = reinterpret_cast<uint16_t*>(slot + ((m * EB + 32 + 15) & ~15u));
+                unsigned char* M = reinterpret_cast<unsigned char*>(P) + ((2 * m + 15) & ~15u);
+                fy_leaf_warp<EB>(slot + a0, P, M, m, q, make_key(K));
+                if (inb) fyn += len;
+            } else if (inb && fy) {
                 fy_leaf<EB>(lb + (x0 & 15u), 0u, (uint32_t)len, start - origin, make_key(key));
                 fyn += len;
             }

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
     for (uint64_t t = gtid(); t < ntiles; t += gstride()) lp.status[t] = 0;
     if (gtid() == 0) {
         lp.ctr->scan_ticket = 0;
+        lp.ctr->nfuse = 0;
         lp.nctr->nseg = 0;
         lp.nctr->nchunk = 0;
     }
@@ -243,7 +244,17 @@ __global__ void k_plan(RunParams rp, LevelParams lp) {
         const SegDesc sg = lp.segs[s];
         uint64_t start, len;
         child_range(sg, lp.prefix, rp.k, b, start, len);
-        if (len <= rp.S_fuse) continue;  // finished by k_finish_children
+        if (len <= rp.S_fuse) {  // finished by k_finish_children (or the leaf kernel)
+            if (rp.max_fused && len > rp.L) {
+                const bool permutes = next < rp.max_levels;  // not a leaf: another level to run
+                if (permutes || lp.dst != rp.buf0) {
+                    const uint32_t at = atomicAdd(&lp.ctr->nfuse, 1u);
+                    if (at < rp.max_fused) rp.fused[at] = (uint32_t)i;
+                    else latch_error(rp.hdr, 4u);
+                }
+            }
+            continue;
+        }
         if (next >= rp.max_levels) continue;  // debug level limit: copied out by k_finish_children
         if (next >= rp.planned_levels) {
             latch_error(rp.hdr, 5u /*SHUF_ERR_DEPTH*/);

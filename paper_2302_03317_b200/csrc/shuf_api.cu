@@ -121,6 +121,9 @@ static void compute_layout(shuf_plan_s* p) {
     l.max_items = n / ((uint64_t)p->L + 1) + 1;
     l.items = off;
     off = align_up(off + l.max_items * item_rec_stride(p->k), 256);
+    l.max_fused = n / ((uint64_t)p->L + 1) + 1;
+    l.fused = off;
+    off = align_up(off + l.max_fused * 4, 256);
     l.total = off;
 }
 
@@ -396,6 +399,8 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     rp.leafk = (uint32_t)p->leafk;
     rp.defer = (uint32_t)p->defer;
     rp.items = sc + p->lay.items;
+    rp.fused = reinterpret_cast<uint32_t*>(sc + p->lay.fused);
+    rp.max_fused = p->leafk ? p->lay.max_fused : 0;  // the list holds children > L only
     {
         const char* dbg = std::getenv("SHUF_DBG");
         rp.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
@@ -499,6 +504,8 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
     rp.defer = 0;
     rp.items = nullptr;
     rp.flags = nullptr;
+    rp.fused = nullptr;
+    rp.max_fused = 0;
     rp.dbg = 0;
     uint64_t launches = 0;
     Prof* prof = nullptr;

@@ -46,7 +46,7 @@ struct LevelCounters {
     uint32_t nseg;
     uint32_t nchunk;
     uint32_t scan_ticket;
-    uint32_t pad;
+    uint32_t nfuse;  // children of this level in the fused list (RunParams::fused)
 };
 
 struct Header {
@@ -77,6 +77,8 @@ struct ScratchLayout {
     uint64_t flags;      // u8 per child of a level: 1 = finished by the general finish kernel
     uint64_t items;      // item records (item_rec_stride bytes each), max_items of them
     uint64_t max_items;
+    uint64_t fused;      // u32 child indices of the current level that the finish kernels take
+    uint64_t max_fused;
     uint64_t total;
     uint64_t max_segs, max_chunks, max_entries, max_tiles;
 };
@@ -105,6 +107,8 @@ struct RunParams {
     uint32_t leafk;         // 1: leaves of HBM levels / user segments go to the leaf kernel (kernels_leaf.cu)
     uint32_t defer;         // 1: the finish leaves the leaves of single-level items to the leaf kernel
     unsigned char* items;   // item records: {start, origin, key} + u16 bucket starts [0, k]
+    uint32_t* fused;        // with the leaf kernel: the level's children that need the finish kernels
+    uint64_t max_fused;     // (k_plan writes them; 0: the finish kernels scan every child)
 };
 
 // Item record of a fused item whose children are all leaves (defer mode):
