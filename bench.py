@@ -252,6 +252,8 @@ def main():
         kernels[name] = d
     dom = max(("scatter", "finish", "leaf"), key=lambda c: prof[c][0])
     dms, dcnt = prof[dom]
+    if dom == "scatter":  # planned-but-empty trailing levels launch and exit at once: count the real ones
+        dcnt = max(1, sum(1 for v in stats["scattered_hbm"] if v > 0))
     achieved = kbytes[dom] / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")

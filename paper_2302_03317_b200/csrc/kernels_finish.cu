@@ -484,13 +484,31 @@ struct ListIter {
     const LevelParams* lp;
     __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {  // warp 0, all lanes
         const uint32_t lane = threadIdx.x & 31u;
+        // 32 entries of this CTA's stride sequence at once: the first one not
+        // taken by k_finish_fast (flag 0) is the next item
+        uint64_t u = ctl->u;
+        uint32_t c = 0;
+        bool found = false;
+        while (u < ctl->units) {
+            const uint64_t ul = u + (uint64_t)lane * gridDim.x;
+            const uint32_t cl = ul < ctl->units ? rp->fused[ul] : 0u;
+            const bool want = ul < ctl->units && !(rp->fast && rp->flags[cl] == 0);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, want);
+            if (bal) {
+                const uint32_t f = __ffs(bal) - 1;
+                c = __shfl_sync(0xFFFFFFFFu, cl, f);
+                u += (uint64_t)(f + 1) * gridDim.x;
+                found = true;
+                break;
+            }
+            u += 32ull * gridDim.x;
+        }
+        __syncwarp();
         if (lane == 0) {
+            ctl->u = u;
             ctl->have[slot] = 0;
             const uint32_t k = rp->k;
-            while (ctl->u < ctl->units) {
-                const uint32_t c = rp->fused[ctl->u];
-                ctl->u += gridDim.x;
-                if (rp->fast && rp->flags[c] == 0) continue;  // taken by k_finish_fast
+            if (found) {
                 const SegDesc sg = lp->segs[c / k];
                 const uint32_t b = c % k;
                 const uint64_t base0 = lp->prefix[sg.cbase];
@@ -503,7 +521,6 @@ struct ListIter {
                 it.origin = sg.origin;
                 it.key = sg.key;
                 ctl->have[slot] = 1;
-                break;
             }
         }
         __syncwarp();

@@ -22,7 +22,7 @@ launches)
   echo "launches exit $?" >> gpurun_out/${TAG}_ncu_launches.log ;;
 full)
   timeout 600 python tools/prof_run.py hot > gpurun_out/${TAG}_plain1.log 2>&1 &&
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_finish_children|k_hist" -c 7 \
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_finish_fast|k_hist" -c 7 \
       -o gpurun_out/${TAG}_full python tools/prof_run.py hot > gpurun_out/${TAG}_ncu_full.log 2>&1
   echo "full exit $?" >> gpurun_out/${TAG}_ncu_full.log ;;
 esac
