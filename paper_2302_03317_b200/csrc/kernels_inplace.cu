@@ -280,77 +280,105 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
 }
 
 // ------------------------------------------------------------------ P2 ----
-template <int EB>
-__device__ __forceinline__ void ip_load_block(typename ElemT<EB>::type* h, const typename ElemT<EB>::type* src) {
-#pragma unroll
-    for (uint32_t e = 0; e < IpCfg<EB>::B; ++e) h[e] = src[e];
-}
-template <int EB>
-__device__ __forceinline__ void ip_store_block(typename ElemT<EB>::type* dst, const typename ElemT<EB>::type* h) {
-#pragma unroll
-    for (uint32_t e = 0; e < IpCfg<EB>::B; ++e) dst[e] = h[e];
-}
+// Every lane is a worker with at most one 128-byte block in hand; a warp
+// moves its lanes' blocks together, one coalesced 128-byte load or store
+// per block (32 lanes x 4 bytes), staging the blocks in hand in shared
+// memory (hand: 32 blocks per warp; tmp: the blocks swapped out).
+constexpr uint32_t kIpPermThreads = 256;
+constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes;  // 64 KiB
 
 template <int EB>
-__global__ void __launch_bounds__(256) k_ip_permute(RunParams rp, IpParams ip) {
-    using E = typename ElemT<EB>::type;
+__global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpParams ip) {
     constexpr uint32_t B = IpCfg<EB>::B;
-    const uint32_t k = rp.k;
-    E* ptr = reinterpret_cast<E*>(rp.buf0);
+    constexpr uint32_t W = kIpBlockBytes / 4;  // 32 words per block
+    const uint32_t k = rp.k, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    unsigned char* base = rp.buf0;
+    uint32_t* hand = reinterpret_cast<uint32_t*>(ism) + warp * (2 * 32 * W);
+    uint32_t* tmp = hand + 32 * W;
     const uint64_t P = (uint64_t)ip.nseg * k;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool done = false;
     if (p >= P) {
-        if (P >= T) return;
-        p %= P;
+        if (P >= T) done = true;
+        else p %= P;
     }
-    E h[B], x[B];
+    bool have = false;
+    uint32_t t = 0;  // bucket of the block in hand
     for (;;) {
-        const uint32_t s = (uint32_t)(p / k);
-        unsigned long long* wrp = (unsigned long long*)&ip.wr[p];
-        const unsigned long long cur = *(volatile unsigned long long*)wrp;
-        bool claimed = false;
-        uint64_t slot = 0;
-        if ((cur & 0xFFFFFFFFull) >= (cur >> 32) + kRBias) {  // r >= w: something may be left
-            const unsigned long long old = atomicAdd(wrp, ~0ull);  // r -= 1
-            const uint64_t ow = old >> 32, orb = old & 0xFFFFFFFFull;
-            if (orb >= ow + kRBias) {
-                claimed = true;
-                slot = orb - kRBias;
+        // ---- A: lanes without a block claim the top unprocessed slot of a region
+        bool need_load = false;
+        const uint32_t* src = nullptr;
+        uint64_t tagi = 0;
+        if (!have && !done) {
+            for (;;) {
+                unsigned long long* wrp = (unsigned long long*)&ip.wr[p];
+                const unsigned long long cur = *(volatile unsigned long long*)wrp;
+                bool claimed = false;
+                uint64_t slot = 0;
+                if ((cur & 0xFFFFFFFFull) >= (cur >> 32) + kRBias) {
+                    const unsigned long long old = atomicAdd(wrp, ~0ull);  // read -= 1
+                    const uint64_t ow = old >> 32, orb = old & 0xFFFFFFFFull;
+                    if (orb >= ow + kRBias) {
+                        claimed = true;
+                        slot = orb - kRBias;
+                    }
+                }
+                if (!claimed) {  // region exhausted: the next pair from the cursor
+                    const uint64_t np = atomicAdd(ip.cursor, 1ull) + (P < T ? P : T);
+                    if (np >= P) {
+                        done = true;
+                        break;
+                    }
+                    p = np;
+                    continue;
+                }
+                const IpSeg sg = ip.segs[(uint32_t)(p / k)];
+                tagi = sg.start / B + slot;
+                const uint32_t tg = ip.tags[tagi];
+                if (tg == kTagEmpty) continue;
+                t = tg;
+                src = reinterpret_cast<const uint32_t*>(base + (sg.start + slot * B) * EB);
+                need_load = true;
+                break;
             }
         }
-        if (!claimed) {  // region exhausted: take the next pair from the cursor
-            const uint64_t np = atomicAdd(ip.cursor, 1ull) + (P < T ? P : T);
-            if (np >= P) return;
-            p = np;
-            continue;
+        const uint32_t ldm = __ballot_sync(0xFFFFFFFFu, need_load);
+        for (uint32_t m = ldm; m; m &= m - 1) {
+            const uint32_t q = __ffs(m) - 1;
+            const uint32_t* sq = reinterpret_cast<const uint32_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)src, q));
+            hand[q * W + lane] = sq[lane];
         }
-        const IpSeg sg = ip.segs[s];
-        const uint64_t tagi = sg.start / B + slot;
-        uint32_t t = ip.tags[tagi];
-        if (t == kTagEmpty) continue;
-        ip_load_block<EB>(h, ptr + sg.start + slot * B);
-        __threadfence();
-        *(volatile uint16_t*)&ip.tags[tagi] = kTagRead;
-        // place the block in hand (bucket t) -- possibly a chain of swaps
-        for (;;) {
+        __syncwarp();
+        if (need_load) {
+            __threadfence();
+            *(volatile uint16_t*)&ip.tags[tagi] = kTagRead;
+            have = true;
+        }
+        // ---- B: place each block in hand at the write pointer of its bucket's region
+        bool swap = false, store = false;
+        uint32_t* dst = nullptr;
+        const uint32_t* ssrc = nullptr;
+        uint32_t t2 = 0;
+        if (have) {
+            const uint32_t s = (uint32_t)(p / k);
+            const IpSeg sg = ip.segs[s];
             const uint64_t q = (uint64_t)s * k + t;
             const unsigned long long old = atomicAdd((unsigned long long*)&ip.wr[q], 1ull << 32);
             const uint64_t ow = old >> 32, orb = old & 0xFFFFFFFFull;
             const bool owned = orb >= ow + kRBias;  // slot ow still unprocessed: ours
             const uint64_t bend = ip.S[(uint64_t)s * (k + 1) + t + 1];
             const uint64_t ti = sg.start / B + ow;
-            E* slotp = ptr + sg.start + ow * B;
-            bool carry_on = false;
+            uint32_t* slotp = reinterpret_cast<uint32_t*>(base + (sg.start + ow * B) * EB);
+            const bool overflow = (ow + 1) * B > bend;
             if (owned) {
-                const uint32_t t2 = ip.tags[ti];
+                t2 = ip.tags[ti];
                 if (t2 != kTagEmpty) {
-                    ip_load_block<EB>(x, slotp);
-                    carry_on = true;
-                    t = t2;
+                    swap = true;
+                    ssrc = slotp;
                 }
-            } else if ((ow + 1) * B <= bend) {
-                // a reader claimed the slot: wait until it has copied the block out
+            } else if (!overflow) {
+                // a reader claimed the slot: wait until its block has been copied out
                 for (;;) {
                     const uint16_t tv = *(volatile uint16_t*)&ip.tags[ti];
                     if (tv == kTagRead || tv == kTagEmpty) break;
@@ -358,17 +386,38 @@ __global__ void __launch_bounds__(256) k_ip_permute(RunParams rp, IpParams ip) {
                 }
                 __threadfence();
             }
-            if ((ow + 1) * B > bend) {
-                // the block would cross the bucket's end: overflow block of (s, bucket)
-                ip_store_block<EB>(reinterpret_cast<E*>(ip.ovfd) + q * B, h);
+            if (overflow) {  // the block would cross its bucket's end: overflow block of (s, bucket)
+                dst = reinterpret_cast<uint32_t*>(ip.ovfd + q * kIpBlockBytes);
                 ip.ovf[q] = 1u;
             } else {
-                ip_store_block<EB>(slotp, h);
+                dst = slotp;
             }
-            if (!carry_on) break;
-#pragma unroll
-            for (uint32_t e = 0; e < B; ++e) h[e] = x[e];
+            store = true;
         }
+        const uint32_t swm = __ballot_sync(0xFFFFFFFFu, swap);
+        for (uint32_t m = swm; m; m &= m - 1) {  // blocks swapped out: read before the stores
+            const uint32_t q = __ffs(m) - 1;
+            const uint32_t* sq = reinterpret_cast<const uint32_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)ssrc, q));
+            tmp[q * W + lane] = sq[lane];
+        }
+        __syncwarp();
+        const uint32_t stm = __ballot_sync(0xFFFFFFFFu, store);
+        for (uint32_t m = stm; m; m &= m - 1) {
+            const uint32_t q = __ffs(m) - 1;
+            uint32_t* dq = reinterpret_cast<uint32_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)dst, q));
+            dq[lane] = hand[q * W + lane];
+        }
+        __syncwarp();
+        for (uint32_t m = swm; m; m &= m - 1) {
+            const uint32_t q = __ffs(m) - 1;
+            hand[q * W + lane] = tmp[q * W + lane];
+        }
+        __syncwarp();
+        if (have) {
+            if (swap) t = t2;
+            else have = false;
+        }
+        if (__ballot_sync(0xFFFFFFFFu, have || !done) == 0) break;
     }
 }
 
@@ -444,15 +493,17 @@ static void* ip_fn(uint32_t eb, int which) {
 }
 
 cudaError_t configure_inplace(uint32_t eb, uint32_t k) {
-    return cudaFuncSetAttribute(ip_fn(eb, 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                ip_classify_smem_bytes(eb, k));
+    cudaError_t e = cudaFuncSetAttribute(ip_fn(eb, 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         ip_classify_smem_bytes(eb, k));
+    if (e) return e;
+    return cudaFuncSetAttribute(ip_fn(eb, 1), cudaFuncAttributeMaxDynamicSharedMemorySize, kIpPermSmem);
 }
 
 cudaError_t occupancy_inplace(uint32_t eb, uint32_t k, int* classify, int* permute) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(classify, ip_fn(eb, 0), kIpThreads,
                                                                   ip_classify_smem_bytes(eb, k));
     if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(permute, ip_fn(eb, 1), 256, 0);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(permute, ip_fn(eb, 1), kIpPermThreads, kIpPermSmem);
 }
 
 cudaError_t launch_ip_stripes(const IpParams& ip, cudaStream_t s) {
@@ -473,7 +524,7 @@ cudaError_t launch_ip_plan(const RunParams& rp, const IpParams& ip, cudaStream_t
 
 cudaError_t launch_ip_permute(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp, (void*)&ip};
-    return cudaLaunchKernel(ip_fn(rp.eb, 1), dim3(grid), dim3(256), args, 0, s);
+    return cudaLaunchKernel(ip_fn(rp.eb, 1), dim3(grid), dim3(kIpPermThreads), args, kIpPermSmem, s);
 }
 
 cudaError_t launch_ip_fill(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
