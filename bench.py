@@ -147,6 +147,17 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(w, n_s):
     import oracle
     a = synth.make_input_np(w, n=n_s)
@@ -154,8 +165,16 @@ def cpu_baseline(w, n_s):
     oracle.shuffle(a, w.k, w.L, w.seed)
     dt = time.perf_counter() - t0
     return {"value": n_s / dt, "unit": "elements/s", "cores": 1, "kind": "oracle",
+            "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
             "sample": f"one oracle shuffle of the first {n_s} elements of the workload "
                       f"({w.note}, k={w.k}, L={w.L}, seed={w.seed}); {dt:.1f} s on 1 host core"}
+
+
+def device_facts(dev) -> dict:
+    import torch
+    pr = torch.cuda.get_device_properties(dev)
+    return {"name": pr.name, "sms": pr.multi_processor_count, "hbm_bytes": pr.total_memory,
+            "l2_bytes": getattr(pr, "L2_cache_size", None), "cc": f"{pr.major}.{pr.minor}"}
 
 
 def main():
@@ -308,7 +327,7 @@ def main():
             "elements_scattered_per_step": scattered, "levels": {"hbm": stats["scattered_hbm"],
                                                                  "smem": stats["scattered_smem"]},
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "device": device_facts(dev),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
