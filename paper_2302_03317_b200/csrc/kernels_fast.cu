@@ -146,6 +146,37 @@ __device__ __forceinline__ void child_of(const LevelParams& lp, uint32_t k, uint
     len = s1 - s0;
 }
 
+// Where the items come from: the children of a stable-mode level (in its
+// output buffer; the stride sequence runs over the fused list when k_plan
+// wrote one) or of an in-place level batch (in ptr, bucket starts from the
+// batch table S).
+struct XSrc {
+    const LevelParams* lp;     // stable mode, or nullptr
+    const IpParams* ip;        // in-place mode
+    const unsigned char* src;  // buffer holding the children
+    uint32_t lvl;              // level of the children
+    uint32_t nchild;           // length of the stride sequence
+    bool copy;                 // src != ptr: non-permuting children must still be copied
+    bool list;                 // the sequence runs over rp.fused
+    __device__ __forceinline__ void child(const RunParams& rp, uint32_t c, uint64_t& start, uint64_t& len,
+                                          uint64_t& origin, uint64_t& key) const {
+        if (lp) {
+            SegDesc sg;
+            child_of(*lp, rp.k, c, start, len, sg);
+            origin = sg.origin;
+            key = sg.key;
+        } else {
+            const uint32_t s = c / rp.k, b = c % rp.k;
+            const uint64_t* S = ip->S + (uint64_t)s * (rp.k + 1);
+            const uint64_t s0 = S[b];
+            start = ip->segs[s].start + s0;
+            len = S[b + 1] - s0;
+            origin = 0;
+            key = rp.seed;  // K(seed, 0) (D2)
+        }
+    }
+};
+
 template <int EB>
 struct XView {
     XLayout Ly;
@@ -203,28 +234,27 @@ __device__ __forceinline__ void c_store(const RunParams& rp, const XView<EB>& V,
 // stride sequence at once (the first taker wins; children before it are
 // flagged, the ones after it are examined again next time).
 template <int EB>
-__device__ __forceinline__ void find_next_warp(const RunParams& rp, const LevelParams& lp, uint32_t nchild,
-                                               XCtl* ctl, uint32_t bi) {
+__device__ __forceinline__ void find_next_warp(const RunParams& rp, const XSrc& xs, uint32_t nchild, XCtl* ctl,
+                                               uint32_t bi) {
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t lvl = lp.level + 1;
+    const uint32_t lvl = xs.lvl;
     uint32_t cursor = ctl->cursor;
     for (;;) {
         if (cursor >= nchild) break;
         const uint64_t c64 = (uint64_t)cursor + (uint64_t)lane * gridDim.x;
         // with the fused list (k_plan) the stride sequence runs over its entries
-        const uint32_t c = (rp.max_fused && c64 < nchild) ? rp.fused[c64] : (uint32_t)c64;
+        const uint32_t c = (xs.list && c64 < nchild) ? rp.fused[c64] : (uint32_t)c64;
         bool take = false;
         int flag = -1;  // -1: leave the flag alone, 0 / 1: write it
-        uint64_t start = 0, len = 0;
-        SegDesc sg;
+        uint64_t start = 0, len = 0, origin = 0, key = 0;
         if (c64 < nchild) {
-            child_of(lp, rp.k, c, start, len, sg);
+            xs.child(rp, c, start, len, origin, key);
             const bool leaf = len <= rp.L;
             if (len == 0 || len > rp.S_fuse || (leaf && rp.leafk)) {
                 // empty, an HBM segment of the next level, or the leaf kernel's
             } else {
                 const bool permutes = (!leaf && lvl < rp.max_levels) || (leaf && rp.run_leaves && len >= 2);
-                if (!permutes) flag = (lp.dst == rp.buf0) ? 0 : 1;
+                if (!permutes) flag = xs.copy ? 1 : 0;
                 else if (leaf || len > XCfg<EB>::SMAX || lvl + 1 > rp.max_levels || !rp.run_leaves) flag = 1;
                 else take = true;
             }
@@ -237,8 +267,8 @@ __device__ __forceinline__ void find_next_warp(const RunParams& rp, const LevelP
                 rp.flags[c] = 0;
                 XItem& it = ctl->item[bi];
                 it.start = start;
-                it.origin = sg.origin;
-                it.key = sg.key;
+                it.origin = origin;
+                it.key = key;
                 it.len = (uint32_t)len;
                 it.child = c;
                 it.valid = 1;
@@ -258,15 +288,15 @@ __device__ __forceinline__ void find_next_warp(const RunParams& rp, const LevelP
 
 // Find the next item, record it for buffer bi and start its load (warp C).
 template <int EB>
-__device__ __forceinline__ void c_load_next(const RunParams& rp, const LevelParams& lp, const XView<EB>& V,
+__device__ __forceinline__ void c_load_next(const RunParams& rp, const XSrc& xs, const XView<EB>& V,
                                             uint32_t nchild, uint32_t bi) {
     const uint32_t lane = threadIdx.x & 31u;
     XCtl* ctl = V.ctl();
-    find_next_warp<EB>(rp, lp, nchild, ctl, bi);
+    find_next_warp<EB>(rp, xs, nchild, ctl, bi);
     __syncwarp();
     const XItem it = ctl->item[bi];
     unsigned char* buf = V.buf(bi);
-    const unsigned char* src = lp.dst;
+    const unsigned char* src = xs.src;
     uint32_t bytes = 0;
     uint64_t A = 0, fl = 0;
     if (it.valid) {
@@ -516,12 +546,12 @@ __device__ __forceinline__ void s_place(const XView<EB>& V, const XItem& it, uns
 
 // ------------------------------------------------------------- kernel ---
 template <int EB, bool NARROW, bool ORD>
-__global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParams lp) {
+__device__ __forceinline__ void run_fast(const RunParams& rp, const XSrc& xs) {
     const XView<EB> V(rp.k);
     XCtl* ctl = V.ctl();
     const uint32_t tid = threadIdx.x, k = rp.k;
-    const uint32_t nchild = rp.max_fused ? lp.ctr->nfuse : lp.ctr->nseg * rp.k;
-    const uint32_t lvl = lp.level + 1;
+    const uint32_t nchild = xs.nchild;
+    const uint32_t lvl = xs.lvl;
     if (tid == 0) {
         ctl->cursor = blockIdx.x;
         ctl->dbg_s = ctl->dbg_f = 0;
@@ -538,8 +568,8 @@ __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParam
     const bool dbgcta = (rp.dbg & 4u) && blockIdx.x == 0;
     if (tid >= XC && tid < XS0) {
         // ---------------- C: loads and stores
-        c_load_next<EB>(rp, lp, V, nchild, 0);
-        c_load_next<EB>(rp, lp, V, nchild, 1);
+        c_load_next<EB>(rp, xs, V, nchild, 0);
+        c_load_next<EB>(rp, xs, V, nchild, 1);
         uint32_t ph[2] = {0, 0};
         for (uint32_t t = 0;; ++t) {
             const uint32_t bi = t & 1u;
@@ -552,7 +582,7 @@ __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParam
                 if (tid == XC) ctl->st_fin += it.len;
             }
             __syncwarp();
-            c_load_next<EB>(rp, lp, V, nchild, bi);
+            c_load_next<EB>(rp, xs, V, nchild, bi);
         }
         if (tid == XC) bulk_wait0();
     } else if (tid >= XS0) {
@@ -633,16 +663,47 @@ __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParam
     }
 }
 
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParams lp) {
+    XSrc xs;
+    xs.lp = &lp;
+    xs.ip = nullptr;
+    xs.src = lp.dst;
+    xs.lvl = lp.level + 1;
+    xs.list = rp.max_fused != 0;
+    xs.nchild = xs.list ? lp.ctr->nfuse : lp.ctr->nseg * rp.k;
+    xs.copy = lp.dst != rp.buf0;
+    run_fast<EB, NARROW, ORD>(rp, xs);
+}
+
+// Children of an in-place level batch (kernels_inplace.cu), in place in ptr.
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(XNT, 1) k_finish_fast_ip(RunParams rp, IpParams ip) {
+    XSrc xs;
+    xs.lp = nullptr;
+    xs.ip = &ip;
+    xs.src = rp.buf0;
+    xs.lvl = ip.level + 1;
+    xs.list = false;
+    xs.nchild = ip.nseg * rp.k;
+    xs.copy = false;
+    run_fast<EB, NARROW, ORD>(rp, xs);
+}
+
 template <int EB>
-static void* fast_fn(bool narrow, bool ord) {
+static void* fast_fn(bool narrow, bool ord, bool ip) {
+    if (ip) {
+        if (ord) return narrow ? (void*)k_finish_fast_ip<EB, true, true> : (void*)k_finish_fast_ip<EB, false, true>;
+        return narrow ? (void*)k_finish_fast_ip<EB, true, false> : (void*)k_finish_fast_ip<EB, false, false>;
+    }
     if (ord) return narrow ? (void*)k_finish_fast<EB, true, true> : (void*)k_finish_fast<EB, false, true>;
     return narrow ? (void*)k_finish_fast<EB, true, false> : (void*)k_finish_fast<EB, false, false>;
 }
-static void* fast_kernel(uint32_t eb, bool narrow, bool ord) {
+static void* fast_kernel(uint32_t eb, bool narrow, bool ord, bool ip = false) {
     switch (eb) {
-    case 4: return fast_fn<4>(narrow, ord);
-    case 8: return fast_fn<8>(narrow, ord);
-    default: return fast_fn<16>(narrow, ord);
+    case 4: return fast_fn<4>(narrow, ord, ip);
+    case 8: return fast_fn<8>(narrow, ord, ip);
+    default: return fast_fn<16>(narrow, ord, ip);
     }
 }
 
@@ -650,11 +711,12 @@ cudaError_t configure_fast(uint32_t eb, uint32_t k) {
     const uint32_t smem = fast_smem_bytes(eb, k);
     if (smem > kSmemLimit) return cudaErrorInvalidValue;
     for (int nr = 0; nr < 2; ++nr)
-        for (int o = 0; o < 2; ++o) {
-            cudaError_t e = cudaFuncSetAttribute(fast_kernel(eb, nr != 0, o != 0),
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e) return e;
-        }
+        for (int o = 0; o < 2; ++o)
+            for (int ip = 0; ip < 2; ++ip) {
+                cudaError_t e = cudaFuncSetAttribute(fast_kernel(eb, nr != 0, o != 0, ip != 0),
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                if (e) return e;
+            }
     return cudaSuccess;
 }
 
@@ -663,6 +725,13 @@ cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaS
     void* args[] = {(void*)&rp, (void*)&lp};
     return cudaLaunchKernel(fast_kernel(rp.eb, rp.bp.narrow != 0, rp.rank_ordered != 0), dim3(grid), dim3(XNT), args,
                             smem, s);
+}
+
+cudaError_t launch_finish_fast_ip(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
+    const uint32_t smem = fast_smem_bytes(rp.eb, rp.k);
+    void* args[] = {(void*)&rp, (void*)&ip};
+    return cudaLaunchKernel(fast_kernel(rp.eb, rp.bp.narrow != 0, rp.rank_ordered != 0, true), dim3(grid), dim3(XNT),
+                            args, smem, s);
 }
 
 }  // namespace shuf

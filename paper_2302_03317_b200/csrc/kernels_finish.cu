@@ -592,6 +592,8 @@ struct IpChildIter {
                 if (len == 0 || len > rp->S_fuse) continue;
                 if (rp->leafk && len <= rp->L) continue;
                 if (!item_permutes(*rp, (uint32_t)len, lvl)) continue;
+                // children taken by k_finish_fast_ip carry flag 0
+                if (rp->fast && rp->flags[(ctl->u / groups) * rp->k + b] == 0) continue;
                 __syncwarp();
                 if (lane == 0) {
                     Item& it = ctl->items[slot];

@@ -44,7 +44,7 @@ namespace shuf {
 extern __shared__ __align__(16) unsigned char ism[];
 
 constexpr uint32_t kIpThreads = 512;   // P1
-constexpr uint32_t kIpTileBytes = 16384;
+constexpr uint32_t kIpTileBytes = 32768;
 constexpr uint16_t kTagEmpty = 0xFFFFu;
 constexpr uint16_t kTagRead = 0xFFFEu;
 constexpr uint64_t kRBias = 1ull << 31;
@@ -271,11 +271,22 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
     }
     __syncthreads();
     const uint64_t nfb = sg.len / B;
+    __shared__ uint32_t work[kMaxK];
     for (uint32_t d = tid; d < k; d += 256) {
         const uint64_t w = (S[d] + B - 1) / B;
         const uint64_t re = min((S[d + 1] + B - 1) / B, nfb);
         const uint64_t r = re + kRBias - 1;  // biased: may sit below w
         ip.wr[(uint64_t)s * k + d] = (w << 32) | (r & 0xFFFFFFFFull);
+        work[d] = re > w ? (uint32_t)(re - w) : 0u;
+    }
+    __syncthreads();
+    if (tid == 0) {  // per-segment prefix of the slots to read (k_ip_permute spreads its workers by it)
+        uint64_t run = 0;
+        for (uint32_t d = 0; d < k; ++d) {
+            run += work[d];
+            ip.regpre[(uint64_t)s * k + d] = (uint32_t)run;
+        }
+        ip.segtot[s] = run;
     }
 }
 
@@ -285,7 +296,7 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
 // per block (32 lanes x 4 bytes), staging the blocks in hand in shared
 // memory (hand: 32 blocks per warp; tmp: the blocks swapped out).
 constexpr uint32_t kIpPermThreads = 256;
-constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes;  // 64 KiB
+constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes + kIpBatchCap * 8;  // 72 KiB
 
 template <int EB>
 __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpParams ip) {
@@ -295,13 +306,41 @@ __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpP
     unsigned char* base = rp.buf0;
     uint32_t* hand = reinterpret_cast<uint32_t*>(ism) + warp * (2 * 32 * W);
     uint32_t* tmp = hand + 32 * W;
+    uint64_t* segpre = reinterpret_cast<uint64_t*>(ism + (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes);
     const uint64_t P = (uint64_t)ip.nseg * k;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool done = false;
-    if (p >= P) {
-        if (P >= T) done = true;
-        else p %= P;
+    // workers spread over the regions in proportion to their unprocessed slots:
+    // worker g starts in the region holding slot g * G / T of the batch
+    if (threadIdx.x == 0) {
+        uint64_t run = 0;
+        for (uint32_t s = 0; s < ip.nseg; ++s) {
+            segpre[s] = run;
+            run += ip.segtot[s];
+        }
+        segpre[ip.nseg] = run;
+    }
+    __syncthreads();
+    const uint64_t G = segpre[ip.nseg];
+    bool done = G == 0;
+    uint64_t p = 0;
+    if (!done) {
+        const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * G / T;
+        uint32_t lo = 0, hi = ip.nseg - 1;  // last segment with segpre <= g
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) / 2;
+            if (segpre[mid] <= g) lo = mid;
+            else hi = mid - 1;
+        }
+        const uint32_t s = lo;
+        const uint32_t gl = (uint32_t)(g - segpre[s]);
+        const uint32_t* rp0 = ip.regpre + (uint64_t)s * k;
+        uint32_t a = 0, b = k - 1;  // first region with inclusive prefix > gl
+        while (a < b) {
+            const uint32_t mid = (a + b) / 2;
+            if (rp0[mid] > gl) b = mid;
+            else a = mid + 1;
+        }
+        p = (uint64_t)s * k + a;
     }
     bool have = false;
     uint32_t t = 0;  // bucket of the block in hand
@@ -324,8 +363,8 @@ __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpP
                         slot = orb - kRBias;
                     }
                 }
-                if (!claimed) {  // region exhausted: the next pair from the cursor
-                    const uint64_t np = atomicAdd(ip.cursor, 1ull) + (P < T ? P : T);
+                if (!claimed) {  // region exhausted: sweep the pairs once more through the cursor
+                    const uint64_t np = atomicAdd(ip.cursor, 1ull);
                     if (np >= P) {
                         done = true;
                         break;

@@ -20,7 +20,7 @@ using namespace shuf;
 
 // Byte offsets of the in-place mode's auxiliary buffer (kernels_inplace.cu).
 struct IpAuxLayout {
-    uint64_t header, ctr, segs[2], zseg, N, F, S, wr, ovf, ovfd, pcnt, part, tags, total;
+    uint64_t header, ctr, segs[2], zseg, N, F, S, wr, regpre, segtot, ovf, ovfd, pcnt, part, tags, flags, total;
     uint64_t Z, max_segs;
     uint32_t cap;
 };
@@ -154,11 +154,14 @@ static void compute_ip_layout(shuf_plan_s* p) {
     l.F = take((uint64_t)l.cap * k * 4);
     l.S = take((uint64_t)l.cap * (k + 1) * 8);
     l.wr = take((uint64_t)l.cap * k * 8);
+    l.regpre = take((uint64_t)l.cap * k * 4);
+    l.segtot = take((uint64_t)l.cap * 8);
     l.ovf = take((uint64_t)l.cap * k * 4);
     l.ovfd = take((uint64_t)l.cap * k * kIpBlockBytes);
     l.pcnt = take((uint64_t)l.cap * k * 4);
     l.part = take((uint64_t)l.cap * k * kIpBlockBytes);
     l.tags = take((n / B + 2) * 2);
+    l.flags = take((uint64_t)l.cap * k);  // per batch child: 1 = the general finish takes it
     l.total = off;
 }
 
@@ -499,11 +502,11 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
     rp.seed = p->seed;
     rp.rank_ordered = (uint32_t)p->rank_ordered;
     rp.fin_nbuf = p->fin_nbuf;
-    rp.fast = 0;
+    rp.fast = (uint32_t)p->fast;
     rp.leafk = 1;
     rp.defer = 0;
     rp.items = nullptr;
-    rp.flags = nullptr;
+    rp.flags = ax + l.flags;
     rp.fused = nullptr;
     rp.max_fused = 0;
     rp.dbg = 0;
@@ -555,6 +558,8 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
             ip.F = reinterpret_cast<uint32_t*>(ax + l.F);
             ip.S = reinterpret_cast<uint64_t*>(ax + l.S);
             ip.wr = reinterpret_cast<uint64_t*>(ax + l.wr);
+            ip.regpre = reinterpret_cast<uint32_t*>(ax + l.regpre);
+            ip.segtot = reinterpret_cast<uint64_t*>(ax + l.segtot);
             ip.ovf = reinterpret_cast<uint32_t*>(ax + l.ovf);
             ip.ovfd = ax + l.ovfd;
             ip.pcnt = reinterpret_cast<uint32_t*>(ax + l.pcnt);
@@ -570,6 +575,7 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
             LAUNCH(SHUF_K_PLAN, launch_ip_plan(rp, ip, st));
             LAUNCH(SHUF_K_SCATTER, launch_ip_permute(rp, ip, st, p->grid_ipp));
             LAUNCH(SHUF_K_SCAN, launch_ip_fill(rp, ip, st, p->grid_ipp));
+            if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast_ip(rp, ip, st, p->grid_fast));
             LAUNCH(SHUF_K_FINISH, launch_finish_ipchildren(rp, ip, st, p->grid_finish));
             LAUNCH(SHUF_K_LEAF, launch_leaf_ipchildren(rp, ip, st, p->grid_leaf));
             s0 = s1;

@@ -159,6 +159,8 @@ struct IpParams {
     uint32_t* F;              // [nseg*k] full blocks per (segment, bucket)
     uint64_t* S;              // [nseg*(k+1)] bucket starts (segment-relative)
     uint64_t* wr;             // [nseg*k] packed (write << 32 | read + 2^31) block pointers
+    uint32_t* regpre;         // [nseg*k] inclusive prefix of the regions' unprocessed slots (per segment)
+    uint64_t* segtot;         // [nseg] unprocessed slots per segment
     uint32_t* ovf;            // [nseg*k] 1: the overflow block of (segment, bucket) is used
     unsigned char* ovfd;      // [nseg*k] overflow blocks
     uint32_t* pcnt;           // [nstripes*k] partial counts
@@ -185,6 +187,7 @@ uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t nb
 uint32_t finish_max_elems(uint32_t eb, uint32_t k);
 uint32_t finish_smem_budget(uint32_t eb);
 cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+cudaError_t launch_finish_fast_ip(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
 cudaError_t configure_fast(uint32_t eb, uint32_t k);
 uint32_t fast_smem_bytes(uint32_t eb, uint32_t k);
 uint32_t fast_max_elems(uint32_t eb);
