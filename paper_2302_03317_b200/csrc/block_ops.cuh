@@ -203,42 +203,83 @@ __device__ __forceinline__ void fy_step(E* A, uint32_t i, uint32_t v, PhiloxKey 
     A[j] = t;
 }
 
+// Partners j_i of the 8 steps i = 8g .. 8g+7 of a leaf (D5: 16-bit lane i&7
+// of the group's Philox block, Lemire16), packed 16 bits per step.  The
+// multiply-shift candidate is exact unless its low half is below s; those
+// rare steps take the exact test (and the retry stream) out of line.
+static __device__ __noinline__ uint4 fy_group_fixup(uint4 pj, uint32_t rej, uint4 w, PhiloxKey key, uint64_t q,
+                                                    uint32_t g) {
+    uint32_t p[4] = {pj.x, pj.y, pj.z, pj.w};
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    for (uint32_t jj = 0; jj < 8; ++jj) {
+        if (!((rej >> jj) & 1u)) continue;
+        const uint32_t v = (wv[jj >> 1] >> ((jj & 1u) * 16u)) & 0xFFFFu;
+        const uint32_t j = fy16_from_lane(v, key, q, g * 8u + jj);
+        const uint32_t sh = (jj & 1u) * 16u;
+        p[jj >> 1] = (p[jj >> 1] & ~(0xFFFFu << sh)) | (j << sh);
+    }
+    return make_uint4(p[0], p[1], p[2], p[3]);
+}
+
+__device__ __forceinline__ uint4 fy_group_partners(uint4 w, PhiloxKey key, uint64_t q, uint32_t g) {
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    uint32_t p[4] = {0u, 0u, 0u, 0u};
+    uint32_t rej = 0;
+#pragma unroll
+    for (uint32_t jj = 0; jj < 8; ++jj) {
+        const uint32_t i = g * 8u + jj, s = i + 1;
+        const uint32_t v = (wv[jj >> 1] >> ((jj & 1u) * 16u)) & 0xFFFFu;
+        const uint32_t mm = v * s;
+        p[jj >> 1] |= (mm >> 16) << ((jj & 1u) * 16u);
+        rej |= (((mm & 0xFFFFu) < s) && i >= 1) ? (1u << jj) : 0u;
+    }
+    uint4 pj = make_uint4(p[0], p[1], p[2], p[3]);
+    if (__builtin_expect(rej != 0, 0)) pj = fy_group_fixup(pj, rej, w, key, q, g);
+    return pj;
+}
+
+// The swaps of one group, steps 8g+7 .. 8g (those in [lo, hi] only when CHECK).
+template <typename E, bool CHECK>
+__device__ __forceinline__ void fy_group_swaps(E* A, uint32_t g, uint4 pj, uint32_t lo, uint32_t hi) {
+    const uint32_t pv[4] = {pj.x, pj.y, pj.z, pj.w};
+#pragma unroll
+    for (int32_t jj = 7; jj >= 0; --jj) {
+        const uint32_t i = g * 8u + (uint32_t)jj;
+        if (CHECK && !(i >= lo && i <= hi)) continue;
+        if (!CHECK && jj == 0 && g == 0) continue;
+        const uint32_t j = (pv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu;
+        const E t = A[i];
+        A[i] = A[j];
+        A[j] = t;
+    }
+}
+
 // Fisher-Yates (Fig. 1) of the leaf A[0 .. cm) whose first
 // element is problem position q: for i = cm-1 .. 1, swap(i, fy(q, i)) with
 // the partner drawn for (leaf id q, step i) (D5): one Philox call per 8
 // steps, so every lane of a warp (each on its own leaf) draws in lockstep.
-// The partial top group is peeled so the full groups run without checks.
+// Partners come a group at a time (branch-free but for rare rejections);
+// the next group's Philox block is computed one group ahead.
 template <int EB>
 __device__ __forceinline__ void fy_leaf(unsigned char* el, uint32_t c, uint32_t cm, uint64_t q, PhiloxKey key) {
     using E = typename ElemT<EB>::type;
     if (cm < 2) return;
     E* A = reinterpret_cast<E*>(el) + c;
     const uint32_t gt = (cm - 1) >> 3;
-    // the next group's Philox block is computed one group ahead so that its
-    // ALU latency overlaps the current group's swaps
     uint4 wn = fy16_group_words(key, q, gt);
     {  // top group: steps cm-1 .. max(8*gt, 1)
-        const uint4 w = wn;
+        const uint4 pj = fy_group_partners(wn, key, q, gt);
         if (gt >= 1) wn = fy16_group_words(key, q, gt - 1);
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int32_t jj = 7; jj >= 0; --jj) {
-            const uint32_t i = gt * 8u + (uint32_t)jj;
-            if (i < cm && i >= 1) fy_step(A, i, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
-        }
+        fy_group_swaps<E, true>(A, gt, pj, 1u, cm - 1);
     }
     for (int32_t g = (int32_t)gt - 1; g >= 1; --g) {  // full groups
-        const uint4 w = wn;
+        const uint4 pj = fy_group_partners(wn, key, q, (uint32_t)g);
         wn = fy16_group_words(key, q, (uint32_t)g - 1u);
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int32_t jj = 7; jj >= 0; --jj)
-            fy_step(A, (uint32_t)g * 8u + (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+        fy_group_swaps<E, false>(A, (uint32_t)g, pj, 0u, 0u);
     }
     if (gt >= 1) {  // group 0: steps 7 .. 1
-        const uint32_t wv[4] = {wn.x, wn.y, wn.z, wn.w};
-#pragma unroll
-        for (int32_t jj = 7; jj >= 1; --jj) fy_step(A, (uint32_t)jj, (wv[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu, key, q);
+        const uint4 pj = fy_group_partners(wn, key, q, 0u);
+        fy_group_swaps<E, false>(A, 0u, pj, 0u, 0u);
     }
 }
 

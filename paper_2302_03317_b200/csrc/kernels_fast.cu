@@ -54,10 +54,13 @@ struct XItem {
     uint32_t len, valid;
 };
 
+constexpr uint32_t XD = 4;  // descriptor ring: item t uses descriptor slot t % XD and buffer t % 2
+
 struct XCtl {
-    XItem item[2];
+    XItem item[XD];
+    uint64_t desc[XD];                      // mbarrier per descriptor slot: published by C
     uint64_t full[2], ready[2], fydone[2];  // mbarriers per buffer
-    uint32_t defer[2];
+    uint32_t defer[XD];
     uint32_t cursor;
     uint32_t dbg_s, dbg_f;
     unsigned long long st_fin, st_fy;
@@ -82,9 +85,9 @@ __host__ __device__ inline XLayout fast_layout(uint32_t eb, uint32_t k) {
     f.buf1 = take(XBUF);
     f.draws = take((narrow ? 1u : 2u) * (smax + 64));
     f.T = take(XSW * (narrow ? k : (k + 1) / 2) * 4);  // narrow: u32 counters, else packed u16
-    f.perm = take(2 * k * 2);                           // per buffer: FY thread -> leaf
-    f.bst0 = take((k + 1) * 4);
-    f.bst1 = take((k + 1) * 4);
+    f.perm = take(XD * k * 2);        // per descriptor slot: FY thread -> leaf
+    f.bst0 = take(XD * (k + 1) * 4);  // per descriptor slot: bucket starts
+    f.bst1 = f.bst0;
     f.wsum = take((XSW + 2 + 32) * 4);
     f.total = off;
     return f;
@@ -186,8 +189,8 @@ struct XView {
     __device__ __forceinline__ unsigned char* buf(uint32_t i) const { return xsm + (i ? Ly.buf1 : Ly.buf0); }
     __device__ __forceinline__ unsigned char* draws() const { return xsm + Ly.draws; }
     __device__ __forceinline__ uint32_t* T() const { return reinterpret_cast<uint32_t*>(xsm + Ly.T); }
-    __device__ __forceinline__ uint32_t* bst(uint32_t i) const {
-        return reinterpret_cast<uint32_t*>(xsm + (i ? Ly.bst1 : Ly.bst0));
+    __device__ __forceinline__ uint32_t* bst(uint32_t d) const {  // d: descriptor slot
+        return reinterpret_cast<uint32_t*>(xsm + Ly.bst0) + d * (k + 1);
     }
     __device__ __forceinline__ uint32_t* wsum() const { return reinterpret_cast<uint32_t*>(xsm + Ly.wsum); }
     __device__ __forceinline__ uint16_t* perm(uint32_t i) const {
@@ -235,7 +238,7 @@ __device__ __forceinline__ void c_store(const RunParams& rp, const XView<EB>& V,
 // flagged, the ones after it are examined again next time).
 template <int EB>
 __device__ __forceinline__ void find_next_warp(const RunParams& rp, const XSrc& xs, uint32_t nchild, XCtl* ctl,
-                                               uint32_t bi) {
+                                               uint32_t ds) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lvl = xs.lvl;
     uint32_t cursor = ctl->cursor;
@@ -265,7 +268,7 @@ __device__ __forceinline__ void find_next_warp(const RunParams& rp, const XSrc& 
         if (tk) {
             if (lane == first) {
                 rp.flags[c] = 0;
-                XItem& it = ctl->item[bi];
+                XItem& it = ctl->item[ds];
                 it.start = start;
                 it.origin = origin;
                 it.key = key;
@@ -280,21 +283,29 @@ __device__ __forceinline__ void find_next_warp(const RunParams& rp, const XSrc& 
         cursor += 32u * gridDim.x;
     }
     if (lane == 0) {
-        ctl->item[bi].valid = 0;
+        ctl->item[ds].valid = 0;
         ctl->cursor = 0xFFFFFFFFu;
     }
     __syncwarp();
 }
 
-// Find the next item, record it for buffer bi and start its load (warp C).
+// Find the next item into descriptor slot ds and publish it (warp C).
 template <int EB>
-__device__ __forceinline__ void c_load_next(const RunParams& rp, const XSrc& xs, const XView<EB>& V,
-                                            uint32_t nchild, uint32_t bi) {
+__device__ __forceinline__ void c_find(const RunParams& rp, const XSrc& xs, const XView<EB>& V, uint32_t nchild,
+                                       uint32_t ds) {
+    XCtl* ctl = V.ctl();
+    find_next_warp<EB>(rp, xs, nchild, ctl, ds);
+    if ((threadIdx.x & 31u) == 0) mbar_arrive1(&ctl->desc[ds]);  // release: the descriptor is written
+    __syncwarp();
+}
+
+// Start the load of the item in descriptor slot ds into buffer bi (warp C);
+// an invalid item completes the buffer's phase with no bytes.
+template <int EB>
+__device__ __forceinline__ void c_load(const XSrc& xs, const XView<EB>& V, uint32_t ds, uint32_t bi) {
     const uint32_t lane = threadIdx.x & 31u;
     XCtl* ctl = V.ctl();
-    find_next_warp<EB>(rp, xs, nchild, ctl, bi);
-    __syncwarp();
-    const XItem it = ctl->item[bi];
+    const XItem it = ctl->item[ds];
     unsigned char* buf = V.buf(bi);
     const unsigned char* src = xs.src;
     uint32_t bytes = 0;
@@ -560,7 +571,10 @@ __device__ __forceinline__ void run_fast(const RunParams& rp, const XSrc& xs) {
             mbar_init(&ctl->full[i], 1);
             mbar_init(&ctl->ready[i], 1);
             mbar_init(&ctl->fydone[i], 1);
-            ctl->defer[i] = 0;
+        }
+        for (uint32_t d = 0; d < XD; ++d) {
+            mbar_init(&ctl->desc[d], 1);
+            ctl->defer[d] = 0;
         }
         fence_mbar_init();
     }
@@ -568,52 +582,55 @@ __device__ __forceinline__ void run_fast(const RunParams& rp, const XSrc& xs) {
     const bool dbgcta = (rp.dbg & 4u) && blockIdx.x == 0;
     if (tid >= XC && tid < XS0) {
         // ---------------- C: loads and stores
-        c_load_next<EB>(rp, xs, V, nchild, 0);
-        c_load_next<EB>(rp, xs, V, nchild, 1);
-        uint32_t ph[2] = {0, 0};
+        // descriptors run up to 4 items ahead of the stores, loads 2 ahead
+        for (uint32_t d = 0; d < XD; ++d) {
+            c_find<EB>(rp, xs, V, nchild, d);
+            if (d < 2) c_load<EB>(xs, V, d, d);
+        }
         for (uint32_t t = 0;; ++t) {
-            const uint32_t bi = t & 1u;
-            mbar_wait(&ctl->fydone[bi], ph[bi]);
-            ph[bi] ^= 1u;
-            const XItem it = ctl->item[bi];
+            const uint32_t bi = t & 1u, ds = t % XD;
+            mbar_wait(&ctl->fydone[bi], (t >> 1) & 1u);
+            const XItem it = ctl->item[ds];
             if (!it.valid) break;
-            if (!ctl->defer[bi]) {
+            if (!ctl->defer[ds]) {
                 c_store<EB>(rp, V, it, bi);
                 if (tid == XC) ctl->st_fin += it.len;
             }
             __syncwarp();
-            c_load_next<EB>(rp, xs, V, nchild, bi);
+            c_load<EB>(xs, V, (t + 2) % XD, bi);  // buffer bi is free: item t+2
+            c_find<EB>(rp, xs, V, nchild, ds);    // descriptor slot ds is free: item t+4
         }
         if (tid == XC) bulk_wait0();
     } else if (tid >= XS0) {
         // ---------------- S: draws, counts, scan, in-place stable scatter
         const uint32_t sid = tid - XS0, w = sid >> 5;
-        uint32_t ph[2] = {0, 0};
         for (uint32_t t = 0;; ++t) {
-            const uint32_t bi = t & 1u;
-            // the descriptor is written before the load is issued: wait for
-            // the load (mbarrier acquire), then read it
-            mbar_wait(&ctl->full[bi], ph[bi]);
-            ph[bi] ^= 1u;
-            const XItem it = ctl->item[bi];
+            const uint32_t bi = t & 1u, ds = t % XD;
+            // draws, counts and scan need only the descriptor: they overlap the load
+            mbar_wait(&ctl->desc[ds], (t / XD) & 1u);
+            const XItem it = ctl->item[ds];
             const bool dbg = dbgcta && sid == 0 && ctl->dbg_s < 40;
             if (dbg) rp.hdr->clk[ctl->dbg_s * 6 + 0] = clock64();
             uint32_t defer = 1;
             if (it.valid && (rp.dbg & 16u)) {  // timing experiment: S does no work (F runs alone)
-                if (sid < k) V.perm(bi)[sid] = (uint16_t)sid;
-                for (uint32_t b = sid; b <= k; b += XSN) V.bst(bi)[b] = (uint32_t)((uint64_t)b * it.len / k);
+                if (sid < k) V.perm(ds)[sid] = (uint16_t)sid;
+                for (uint32_t b = sid; b <= k; b += XSN) V.bst(ds)[b] = (uint32_t)((uint64_t)b * it.len / k);
                 defer = 0;
+                mbar_wait(&ctl->full[bi], (t >> 1) & 1u);
             } else if (it.valid) {
                 s_count<EB, NARROW>(rp, V, it, lvl, w);
                 bar_group(kBarS, XSN);
-                defer = s_scan<EB, NARROW>(rp, V, V.bst(bi), V.perm(bi), it.start, it.len, sid);
+                defer = s_scan<EB, NARROW>(rp, V, V.bst(ds), V.perm(ds), it.start, it.len, sid);
                 if (dbg) rp.hdr->clk[ctl->dbg_s * 6 + 1] = clock64();
+                mbar_wait(&ctl->full[bi], (t >> 1) & 1u);  // the item's data
                 if (!defer) s_place<EB, NARROW, ORD>(V, it, item_base<EB>(V.buf(bi), it.start), w);
                 else if (sid == 0) rp.flags[it.child] = 1;  // the general kernel takes it
+            } else {
+                mbar_wait(&ctl->full[bi], (t >> 1) & 1u);
             }
             bar_group(kBarS, XSN);
             if (sid == 0) {
-                ctl->defer[bi] = defer;
+                ctl->defer[ds] = defer;
                 if (dbg) rp.hdr->clk[ctl->dbg_s++ * 6 + 2] = clock64();
                 mbar_arrive1(&ctl->ready[bi]);
             }
@@ -621,21 +638,19 @@ __device__ __forceinline__ void run_fast(const RunParams& rp, const XSrc& xs) {
         }
     } else {
         // ---------------- F: Fisher-Yates of every leaf of item t
-        uint32_t ph[2] = {0, 0};
         unsigned long long fyn = 0;
         for (uint32_t t = 0;; ++t) {
-            const uint32_t bi = t & 1u;
-            mbar_wait(&ctl->ready[bi], ph[bi]);
-            ph[bi] ^= 1u;
-            const XItem it = ctl->item[bi];
+            const uint32_t bi = t & 1u, ds = t % XD;
+            mbar_wait(&ctl->ready[bi], (t >> 1) & 1u);
+            const XItem it = ctl->item[ds];
             const bool dbg = dbgcta && tid == 0 && ctl->dbg_f < 40;
             if (dbg) rp.hdr->clk[ctl->dbg_f * 6 + 3] = clock64();
-            if (it.valid && !ctl->defer[bi] && !(rp.dbg & 8u)) {  // dbg 8: timing experiment, no FY
-                const uint32_t* bst = V.bst(bi);
+            if (it.valid && !ctl->defer[ds] && !(rp.dbg & 8u)) {  // dbg 8: timing experiment, no FY
+                const uint32_t* bst = V.bst(ds);
                 unsigned char* base = item_base<EB>(V.buf(bi), it.start);
                 const uint64_t P0 = it.start - it.origin;
                 const PhiloxKey key = make_key(it.key);
-                const uint16_t* perm = V.perm(bi);
+                const uint16_t* perm = V.perm(ds);
                 for (uint32_t f = tid; f < k; f += XF) {
                     const uint32_t b = (k <= XF) ? perm[f] : f;
                     const uint32_t s0 = bst[b], cm = bst[b + 1] - s0;
