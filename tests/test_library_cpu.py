@@ -65,6 +65,21 @@ def test_plan_scratch_and_levels(L):
     assert big.scratch_bytes >= (1 << 32) * 16
 
 
+@pytest.mark.parametrize("n,eb,k,L_", [(1 << 30, 4, 256, 4096), (1 << 27, 4, 256, 4096), (1_000_000_007, 8, 256, 2048),
+                                        (1 << 32, 16, 1024, 2048), (1 << 20, 4, 256, 4096), (100_000, 4, 2, 1)])
+def test_inplace_aux_is_a_small_fraction(n, eb, k, L_):
+    """The in-place mode's aux memory is a few percent of
+    the data (plus a fixed part for the batch buffers, <= 96 MiB) -- the point
+    of the mode -- while the stable mode's scratch holds a full ping-pong copy."""
+    p = shuf.shuf_plan(n, eb, k, L_, 1)
+    aux = shuf.shuf_aux_bytes_inplace(p)
+    assert aux > 0
+    assert aux < 0.05 * n * eb + (96 << 20), (aux, n * eb)
+    if n * eb >= (1 << 30):
+        assert aux < 0.05 * n * eb, (aux, n * eb)
+    assert p.scratch_bytes >= n * eb
+
+
 def test_status_strings(L):
     for c in range(7):
         assert L.shuf_status_string(c)
