@@ -729,7 +729,7 @@ cudaError_t configure_fast(uint32_t eb, uint32_t k) {
         for (int o = 0; o < 2; ++o)
             for (int ip = 0; ip < 2; ++ip) {
                 cudaError_t e = cudaFuncSetAttribute(fast_kernel(eb, nr != 0, o != 0, ip != 0),
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
                 if (e) return e;
             }
     return cudaSuccess;

@@ -766,16 +766,16 @@ cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t configure_finish(uint32_t smem) {
+cudaError_t configure_finish(uint32_t) {  // the attribute is the limit: plans of other sizes share the kernels
     for (uint32_t eb : {4u, 8u, 16u})
         for (int seg = 0; seg < 2; ++seg)
             for (int nr = 0; nr < 2; ++nr)
                 for (int o = 0; o < 2; ++o) {
                     cudaError_t e = cudaFuncSetAttribute(fin_fn(eb, seg, nr, o),
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
                     if (e) return e;
                     if (seg == 0 && (e = cudaFuncSetAttribute(fin_ip(eb, nr, o),
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)))
                         return e;
                 }
     return cudaSuccess;

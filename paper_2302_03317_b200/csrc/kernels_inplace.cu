@@ -532,10 +532,9 @@ static void* ip_fn(uint32_t eb, int which) {
 }
 
 cudaError_t configure_inplace(uint32_t eb, uint32_t k) {
-    cudaError_t e = cudaFuncSetAttribute(ip_fn(eb, 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ip_classify_smem_bytes(eb, k));
+    cudaError_t e = cudaFuncSetAttribute(ip_fn(eb, 0), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e) return e;
-    return cudaFuncSetAttribute(ip_fn(eb, 1), cudaFuncAttributeMaxDynamicSharedMemorySize, kIpPermSmem);
+    return cudaFuncSetAttribute(ip_fn(eb, 1), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
 }
 
 cudaError_t occupancy_inplace(uint32_t eb, uint32_t k, int* classify, int* permute) {

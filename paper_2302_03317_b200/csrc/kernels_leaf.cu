@@ -344,9 +344,9 @@ static void* leaf_fn(uint32_t eb, int mode) {
 }
 
 cudaError_t configure_leaf(uint32_t eb, uint32_t L) {
-    const uint32_t smem = leaf_smem_bytes(eb, L);
+    (void)L;  // the attribute is the limit: plans of other sizes share the kernels
     for (int mode = 0; mode < 4; ++mode) {
-        cudaError_t e = cudaFuncSetAttribute(leaf_fn(eb, mode), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(leaf_fn(eb, mode), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
         if (e) return e;
     }
     return cudaSuccess;

@@ -365,13 +365,13 @@ cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStrea
                             dim3(kSW * 32), args, smem, s);
 }
 
-cudaError_t configure_scatter(uint32_t smem) {
+cudaError_t configure_scatter(uint32_t) {  // the attribute is the limit: plans with other sizes share the kernels
     cudaError_t e;
     for (uint32_t eb : {4u, 8u, 16u})
         for (int o = 0; o < 2; ++o)
             for (int nr = 0; nr < 2; ++nr)
                 if ((e = cudaFuncSetAttribute(scatter_kernel(eb, o, nr), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              smem)))
+                                              kSmemLimit)))
                     return e;
     return cudaSuccess;
 }

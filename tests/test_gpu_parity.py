@@ -115,6 +115,26 @@ def test_repeat_runs_identical_and_stream_independent():
     assert (np.sort(r1) == a).all()
 
 
+def test_interleaved_plans_share_kernels():
+    """Plans of different shapes (k, element size, fused size) used in turn
+    in one process: the kernels' shared-memory limits are process-wide, so a
+    plan set up later must not break an earlier one."""
+    a = np.arange(3_000_000, dtype=np.uint32)
+    b = synth.splitmix64_stream_np(3, 0, 400_000)
+    c = np.arange(300_001, dtype=np.uint32)
+    shapes = [(a, 256, 4096, 11), (b, 1000, 50, 7), (c, 2, 1, 8)]
+    plans = []
+    for arr, k, L, seed in shapes:
+        p = shuf.shuf_plan(arr.shape[0], arr.dtype.itemsize, k, L, seed)
+        plans.append((p, torch.empty(p.scratch_bytes, dtype=torch.uint8, device="cuda")))
+    for rnd in range(2):
+        for (arr, k, L, seed), (p, scr) in zip(shapes, plans):
+            x = to_dev(arr)
+            shuf.shuf_run(p, x, scr)
+            assert shuf.shuf_last_device_error(p) == 0
+            assert (to_host(x, arr) == oracle.shuffle(arr, k, L, seed)).all(), (k, L, rnd)
+
+
 def test_documented_match_rank_path_bit_exact():
     """The ranking fallback (__match_any_sync, SHUF_RANK_MODE=match) is chosen
     once per process, so it runs in a subprocess over every path: HBM levels,
