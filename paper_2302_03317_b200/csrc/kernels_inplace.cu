@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
 // per block (32 lanes x 4 bytes), staging the blocks in hand in shared
 // memory (hand: 32 blocks per warp; tmp: the blocks swapped out).
 constexpr uint32_t kIpPermThreads = 256;
-constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes + kIpBatchCap * 8;  // 72 KiB
+constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes + (kIpBatchCap + 1) * 8;  // ~72 KiB
 
 template <int EB>
 __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpParams ip) {
