@@ -134,11 +134,16 @@ static void compute_ip_layout(shuf_plan_s* p) {
     IpAuxLayout& l = p->ipl;
     const uint64_t n = p->n, k = p->k;
     const uint64_t B = kIpBlockBytes / p->eb;
-    l.Z = align_up((n + kIpBatchCap - 1) / kIpBatchCap, 4096);
+    // batch capacity: the per-(stripe|segment, bucket) buffers (~2 blocks + 32 B each) stay within
+    // ~4 % of the data plus 32 MiB, and between 64 and kIpBatchCap entries
+    const uint64_t per = k * (2 * kIpBlockBytes + 32);
+    uint64_t capb = (n * p->eb / 25 + (32ull << 20)) / per;
+    capb = capb < 64 ? 64 : (capb > kIpBatchCap ? kIpBatchCap : capb);
+    l.Z = align_up((n + capb - 1) / capb, 4096);
     if (l.Z < 65536) l.Z = 65536;
     l.max_segs = n / ((uint64_t)p->S_fuse + 1) + 1;
     uint64_t cap = n / l.Z + l.max_segs + 1;
-    l.cap = (uint32_t)(cap < kIpBatchCap ? cap : kIpBatchCap);
+    l.cap = (uint32_t)(cap < capb ? cap : capb);
     uint64_t off = 0;
     auto take = [&off](uint64_t bytes) {
         const uint64_t at = off;

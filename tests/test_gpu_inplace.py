@@ -60,8 +60,8 @@ def test_inplace_bijection_and_level0_buckets(n, k, L, seed):
     a = np.arange(n, dtype=np.uint32)
     got, plan = gpu_inplace(a, k, L, seed)
     assert (np.sort(got) == a).all()
-    # aux is a small fraction of the data
-    assert shuf.shuf_aux_bytes_inplace(plan) < max(4 * n, 64 << 20)
+    # aux is a small fraction of the data plus a bounded fixed part
+    assert shuf.shuf_aux_bytes_inplace(plan) < 0.05 * 4 * n + (96 << 20)
     # every level-0 bucket range holds exactly the stable mode's elements
     bnd = level0_bounds(n, k, seed)
     exp = oracle.shuffle(a, k, L, seed)
