@@ -56,6 +56,8 @@ CASES = [
     (200_000, 2, 1, 8, 4),                                              # deepest recursion
     (123_457, 64, 2048, 9, 8), (99_991, 1024, 2048, 10, 16),            # element sizes
     (3_000_000, 256, 4096, 11, 4),                                      # 2 global levels
+    (2_000_000, 256, 1000, 12, 8), (1_000_000, 256, 500, 13, 16),       # fused items of 8/16-byte elements
+    (1_500_000, 1024, 600, 14, 16),                                     # k = 1024: several leaves per FY thread
 ]
 
 
