@@ -53,10 +53,12 @@ typedef enum {
 /* Create a plan for shuffling n elements of elem_bytes bytes each with k
  * buckets per scatter level, leaves of at most L elements, and seed `seed`
  * (D2: the single-problem key is K = seed).
- * Domain: elem_bytes in {4, 8, 16}; 2 <= k <= 4096 (any k; powers of two take
- * the shift path of P:99); 1 <= L <= the device leaf capacity (L*elem_bytes
- * <= 96 KiB).  n may be 0 or 1 (no-ops).  For shuf_segmented, n is the total
- * number of elements over all segments.
+ * Domain: elem_bytes in {4, 8, 16}; 2 <= k <= 1024 on the device (any k;
+ * powers of two <= 256 take the 8-bit-lane shift path of P:99; larger k
+ * return SHUF_ERR_UNSUPPORTED); 1 <= L <= the fused size S_fuse (about 20 K
+ * 4-byte, 11 K 8-byte or 6 K 16-byte elements; larger L return
+ * SHUF_ERR_UNSUPPORTED).  n may be 0 or 1 (no-ops); n is 64-bit.  For
+ * shuf_segmented, n is the total number of elements over all segments.
  * Returns NULL on error; the reason is in shuf_last_status(). */
 shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, uint32_t L, uint64_t seed);
 

@@ -65,7 +65,8 @@ __host__ __device__ inline SLayout s_layout(uint32_t k) {
     L.tab = take(kSW * (narrow ? k : (k + 1) / 2) * 4);  // u32 counters (narrow k) or packed u16 pairs
     L.bst = take((k + 1) * 4);
     L.run = take(k * 8);
-    L.delta = take(k * 4);  // u32: destination minus slot, relative to the segment start (mod 2^32)
+    L.delta = take(k * 8);  // destination minus slot: u32 relative to the segment start (mod 2^32),
+                            // u64 absolute for segments longer than 2^32 elements
     L.wsum = take((kSW + 1) * 4);
     L.bar = take(16);
     L.total = off;
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
     uint32_t* bst = reinterpret_cast<uint32_t*>(sm + Ly.bst);
     uint64_t* running = reinterpret_cast<uint64_t*>(sm + Ly.run);
     uint32_t* delta = reinterpret_cast<uint32_t*>(sm + Ly.delta);
+    uint64_t* delta64 = reinterpret_cast<uint64_t*>(sm + Ly.delta);
     D* slotb = reinterpret_cast<D*>(sm + Ly.slotb);
     uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + Ly.wsum);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + Ly.bar);
@@ -317,10 +319,13 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
             }
         }
         // destinations of the tile's runs: dst index of slot s = delta[b] + s
-        // segments hold <= 2^32 elements, so every destination minus the segment
-        // start fits 32 bits: delta is kept modulo 2^32
+        // a segment of <= 2^32 elements: every destination minus the segment
+        // start fits 32 bits, so delta is kept modulo 2^32 (half the lookup
+        // bytes in the copy-out); longer segments keep 64-bit deltas
+        const bool wide = (sg.len >> 32) != 0;
         for (uint32_t b = tid; b < k; b += kSW * 32) {
-            delta[b] = (uint32_t)(running[b] - sg.start) - bst[b];
+            if (wide) delta64[b] = running[b] - bst[b];
+            else delta[b] = (uint32_t)(running[b] - sg.start) - bst[b];
             running[b] += bst[b + 1] - bst[b];
         }
         __syncthreads();
@@ -330,9 +335,14 @@ __global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelPara
         //      1-3 runs that meet its 32 slots (coalesced)
         {
             const E* el = reinterpret_cast<const E*>(buf + ((cur.q0 * EB) & 15u));
-            E* dst = reinterpret_cast<E*>(dstb) + sg.start;
+            if (!wide) {
+                E* dst = reinterpret_cast<E*>(dstb) + sg.start;
 #pragma unroll 4
-            for (uint32_t x = tid; x < cnt; x += kSW * 32) dst[(uint32_t)(delta[slotb[x]] + x)] = el[x];
+                for (uint32_t x = tid; x < cnt; x += kSW * 32) dst[(uint32_t)(delta[slotb[x]] + x)] = el[x];
+            } else {
+                E* dst = reinterpret_cast<E*>(dstb);
+                for (uint32_t x = tid; x < cnt; x += kSW * 32) dst[delta64[slotb[x]] + x] = el[x];
+            }
         }
         __syncthreads();
         if (dbg) rp.hdr->sclk[it * 6 + 5] = clock64();
