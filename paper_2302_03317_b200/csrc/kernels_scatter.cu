@@ -30,11 +30,11 @@
 
 namespace shuf {
 
-constexpr uint32_t kSW = 8;  // warps per CTA: 256 threads, 3 CTAs per SM
+constexpr uint32_t kSW = 8;  // warps per CTA: 256 threads, 2 CTAs per SM (32 KiB tiles)
 
 template <int EB>
 struct SCfg {
-    static constexpr uint32_t T = kScatterTileBytes / EB;  // elements per tile (24 KiB)
+    static constexpr uint32_t T = kScatterTileBytes / EB;  // elements per tile (32 KiB)
 };
 
 // Draw storage of a tile: one 16-byte slot per Philox group (+1 for the
@@ -131,7 +131,7 @@ __device__ __forceinline__ void s_issue_load(uint64_t q0, uint32_t cnt, const un
 }
 
 template <int EB, bool ORD, bool NARROW>
-__global__ void __launch_bounds__(kSW * 32, 3) k_scatter(RunParams rp, LevelParams lp) {
+__global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelParams lp) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
     constexpr uint32_t T = SCfg<EB>::T;

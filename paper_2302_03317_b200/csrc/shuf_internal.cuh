@@ -17,7 +17,7 @@ constexpr uint32_t kSmemLimit = 227 * 1024;
 constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
 constexpr uint32_t kSegGroup = 8;          // user segments per finish work unit (segmented mode)
 constexpr uint32_t kMaxLevels = 256;
-constexpr uint32_t kScatterTileBytes = 24576; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
+constexpr uint32_t kScatterTileBytes = 32768; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
 constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
 constexpr uint32_t kIpBlockBytes = 128;     // in-place mode block (kernels_inplace.cu)
 constexpr uint32_t kIpBatchCap = 1024;      // in-place mode: stripes (and segments) per batch
