@@ -121,3 +121,33 @@ def test_c4_records_bijection_and_payload():
         assert bool((synth.splitmix64_of_torch(key) == x[s:s + step, 1]).all())
         seen[key] = True
     assert bool(seen.all())
+
+
+def test_c4_inplace_bijection_payload_and_block_chi2():
+    """BASELINE config 4 asks for the in-place mode at full size too (SURVEY
+    8(c) Q14): 2^32 16-byte records shuffled with ~1.4 GB of aux instead of a
+    64 GiB ping-pong buffer; every key exactly once with its payload, and the
+    one-run (source block, destination block) table over a 64 x 64 grid is
+    uniform (chi^2, 3969 dof; each cell expects 2^20 records)."""
+    from scipy import stats
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    w = synth.WORKLOADS["c4"]
+    if free < w.n * w.elem_bytes + (16 << 30):
+        pytest.skip("needs ~80 GB of free device memory")
+    x = synth.make_input_torch(w, DEV)
+    shuf.inplace_shuffle(x, w.k, w.L, w.seed, elem_bytes=w.elem_bytes)
+    seen = torch.zeros(w.n, dtype=torch.bool, device=DEV)
+    table = torch.zeros(64 * 64, dtype=torch.int64, device=DEV)
+    step = 1 << 28
+    for s in range(0, w.n, step):
+        key = x[s:s + step, 0]
+        assert bool((synth.splitmix64_of_torch(key) == x[s:s + step, 1]).all())
+        seen[key] = True
+        src = (key.to(torch.int64) & 0xFFFFFFFF) * 64 // w.n
+        dst = torch.arange(s, s + key.numel(), device=DEV, dtype=torch.int64) * 64 // w.n
+        table += torch.bincount(src * 64 + dst, minlength=64 * 64)
+    assert bool(seen.all())
+    assert stats.chisquare(table.cpu().numpy()).pvalue > 0.001
