@@ -46,8 +46,6 @@ struct XCfg {
     static constexpr uint32_t R = (SMAX + 16 * XSW) / (32 * XSW) + 2;  // rounds per S warp
 };
 
-uint32_t fast_max_elems(uint32_t eb) { return XIN / eb; }
-
 struct XItem {
     uint64_t start, origin, key;
     uint64_t child;  // child index c = s*k + b (for the deferral flag)

@@ -15,7 +15,6 @@ constexpr uint32_t kMaxK = 1024;           // device bucket-count limit
 constexpr uint32_t kScanTile = 4096;       // entries per decoupled-lookback tile
 constexpr uint32_t kSmemLimit = 227 * 1024;
 constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
-constexpr uint32_t kSegGroup = 8;          // user segments per finish work unit (segmented mode)
 constexpr uint32_t kMaxLevels = 256;
 constexpr uint32_t kScatterTileBytes = 32768; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
 constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
@@ -190,7 +189,6 @@ cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaS
 cudaError_t launch_finish_fast_ip(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
 cudaError_t configure_fast(uint32_t eb, uint32_t k);
 uint32_t fast_smem_bytes(uint32_t eb, uint32_t k);
-uint32_t fast_max_elems(uint32_t eb);
 cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
                                  cudaStream_t s, int grid);
