@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
 // per block (32 lanes x 4 bytes), staging the blocks in hand in shared
 // memory (hand: 32 blocks per warp; tmp: the blocks swapped out).
 constexpr uint32_t kIpPermThreads = 256;
-constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes + (kIpBatchCap + 1) * 8;  // ~72 KiB
+constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 32 * kIpBlockBytes + (kIpBatchCap + 1) * 8;  // ~40 KiB
 
 template <int EB>
 __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpParams ip) {
@@ -304,9 +304,8 @@ __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpP
     constexpr uint32_t W = kIpBlockBytes / 4;  // 32 words per block
     const uint32_t k = rp.k, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     unsigned char* base = rp.buf0;
-    uint32_t* hand = reinterpret_cast<uint32_t*>(ism) + warp * (2 * 32 * W);
-    uint32_t* tmp = hand + 32 * W;
-    uint64_t* segpre = reinterpret_cast<uint64_t*>(ism + (kIpPermThreads / 32) * 2 * 32 * kIpBlockBytes);
+    uint32_t* hand = reinterpret_cast<uint32_t*>(ism) + warp * (32 * W);
+    uint64_t* segpre = reinterpret_cast<uint64_t*>(ism + (kIpPermThreads / 32) * 32 * kIpBlockBytes);
     const uint64_t P = (uint64_t)ip.nseg * k;
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
     // workers spread over the regions in proportion to their unprocessed slots:
@@ -433,13 +432,18 @@ __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpP
             }
             store = true;
         }
+        // blocks swapped out are read before the stores, into registers (lane l
+        // holds word l of every swapped block: tr[q] for the block of lane q)
         const uint32_t swm = __ballot_sync(0xFFFFFFFFu, swap);
-        for (uint32_t m = swm; m; m &= m - 1) {  // blocks swapped out: read before the stores
-            const uint32_t q = __ffs(m) - 1;
-            const uint32_t* sq = reinterpret_cast<const uint32_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)ssrc, q));
-            tmp[q * W + lane] = sq[lane];
+        uint32_t tr[32];
+        if (swm) {
+#pragma unroll
+            for (uint32_t q = 0; q < 32; ++q) {
+                const uint32_t* sq =
+                    reinterpret_cast<const uint32_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)ssrc, q));
+                if ((swm >> q) & 1u) tr[q] = sq[lane];
+            }
         }
-        __syncwarp();
         const uint32_t stm = __ballot_sync(0xFFFFFFFFu, store);
         for (uint32_t m = stm; m; m &= m - 1) {
             const uint32_t q = __ffs(m) - 1;
@@ -447,9 +451,10 @@ __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpP
             dq[lane] = hand[q * W + lane];
         }
         __syncwarp();
-        for (uint32_t m = swm; m; m &= m - 1) {
-            const uint32_t q = __ffs(m) - 1;
-            hand[q * W + lane] = tmp[q * W + lane];
+        if (swm) {
+#pragma unroll
+            for (uint32_t q = 0; q < 32; ++q)
+                if ((swm >> q) & 1u) hand[q * W + lane] = tr[q];
         }
         __syncwarp();
         if (have) {
