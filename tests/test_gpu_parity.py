@@ -175,6 +175,10 @@ _ENV_CASES = (
     "off = np.array([0, 0, 1, 3000, 3000, 9000, 9001, 60000, 64000], dtype=np.uint64)\n"
     "c = np.arange(int(off[-1]), dtype=np.uint32)\n"
     "assert (gpu_segmented(c, off, 64, 4096, 5) == oracle.segmented(c, off, 64, 4096, 5)).all()\n"
+    "import torch, paper_2302_03317_b200 as shuf\n"
+    "d = torch.arange(3_000_000, dtype=torch.int32, device='cuda')\n"
+    "shuf.inplace_shuffle(d, 256, 4096, 11)\n"
+    "assert (torch.sort(d)[0] == torch.arange(3_000_000, dtype=torch.int32, device='cuda')).all()\n"
     "print('ok')\n")
 
 
