@@ -115,8 +115,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
             const uint64_t pb = g << sh;
             if (pb >= P0 && pb + dpg <= P1) {
                 if (bp.narrow) {
+                    // the 16 draws are the bytes of the group's words shifted right by
+                    // 8 - log2 k (masked per byte): one byte extract each
+                    const uint32_t msk = (0xFFu >> bp.shift) * 0x01010101u;
+                    const uint32_t pw[4] = {(w.x >> bp.shift) & msk, (w.y >> bp.shift) & msk,
+                                            (w.z >> bp.shift) & msk, (w.w >> bp.shift) & msk};
 #pragma unroll
-                    for (uint32_t jj = 0; jj < 16; ++jj) atomicAdd(&hist[lane8(w, jj) >> bp.shift], 1u);
+                    for (uint32_t jj = 0; jj < 16; ++jj)
+                        atomicAdd(&hist[__byte_perm(pw[jj >> 2], 0u, 0x4440u | (jj & 3u))], 1u);
                 } else {
 #pragma unroll
                     for (uint32_t jj = 0; jj < 8; ++jj)
