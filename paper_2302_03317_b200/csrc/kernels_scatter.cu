@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelPara
 #pragma unroll
                     for (uint32_t j = 0; j < dpg; ++j) {
                         if (NARROW) {
-                            atomicAdd(&Tw[(pw4[j >> 2] >> ((j & 3u) * 8u)) & 0xFFu], 1u);
+                            atomicAdd(&Tw[__byte_perm(pw4[j >> 2], 0u, 0x4440u | (j & 3u))], 1u);
                         } else {
                             const uint32_t b = (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
                             atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
