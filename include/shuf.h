@@ -155,10 +155,13 @@ shuf_status shuf_profile_run(shuf_plan_t p, void *ptr, const uint64_t *d_offsets
  * Writes min(count, 515) entries; the rest are zero. */
 shuf_status shuf_last_run_stats(shuf_plan_t p, void *stream, uint64_t *out, uint32_t count);
 
-/* Debug: phase timestamps (clock64) recorded by CTA 0 of the fast finish
- * kernel during the last run on this plan (6 per item) in out[0, 256) and
- * by CTA 0 of the level-0 HBM scatter (6 per tile) in out[256, 512);
- * writes min(count, 512) values.  Synchronises. */
+/* Debug (timing experiments; recorded only when the environment variable
+ * SHUF_DBG selects them): phase timestamps (clock64) of CTA 0 of the finish
+ * kernels during the last run on this plan (6 per item; SHUF_DBG=4 the
+ * pipelined finish's S/F groups, SHUF_DBG=2 the general finish) in
+ * out[0, 256) and of CTA 0 of the level-0 HBM scatter (6 per tile,
+ * SHUF_DBG=1) in out[256, 512); writes min(count, 512) values.
+ * Synchronises. */
 shuf_status shuf_debug_clocks(shuf_plan_t p, void *stream, long long *out, uint32_t count);
 
 /* Synchronise `stream` and return the plan's latched device error (SHUF_OK

@@ -731,13 +731,13 @@ extern "C" const char* shuf_status_string(shuf_status s) {
     return "unknown status";
 }
 
-// Debug: phase clocks recorded by CTA 0 of the fast finish (kernels_fast.cu).
+// Debug: phase clocks recorded by CTA 0 of the finish kernels / the level-0 scatter (SHUF_DBG).
 extern "C" shuf_status shuf_debug_clocks(shuf_plan_t p, void* stream, long long* out, uint32_t count) {
     if (!p || !out) return SHUF_ERR_INVALID_ARG;
     if (!p->last_hdr) return SHUF_OK;
     cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
     if (e) return cuda_fail(p, e);
-    if (count > 512) count = 512;  // [0, 256): fast finish, [256, 512): level-0 scatter
+    if (count > 512) count = 512;  // [0, 256): finish, [256, 512): level-0 scatter
     if ((e = cudaMemcpy(out, p->last_hdr->clk, count * sizeof(long long), cudaMemcpyDeviceToHost))) return cuda_fail(p, e);
     return SHUF_OK;
 }
