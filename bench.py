@@ -217,7 +217,8 @@ def main():
         d_off = None
         x = synth.make_input_torch(w, dev)
     plan = shuf.shuf_plan(w.n, w.elem_bytes, w.k, w.L, seed)
-    scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(plan.scratch_bytes if d_off is None else plan.scratch_bytes_segmented(d_off.numel() - 1),
+                          dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():

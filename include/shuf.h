@@ -47,7 +47,10 @@ typedef enum {
     SHUF_ERR_ALIGNMENT = 3,   /* ptr/scratch/offsets not 16-byte aligned         */
     SHUF_ERR_SCRATCH = 4,     /* scratch_bytes smaller than shuf_scratch_bytes() */
     SHUF_ERR_DEPTH = 5,       /* more levels than planned (device-detected)      */
-    SHUF_ERR_CUDA = 6         /* a CUDA runtime error; see shuf_last_cuda_error  */
+    SHUF_ERR_CUDA = 6,        /* a CUDA runtime error; see shuf_last_cuda_error  */
+    SHUF_ERR_RANK_ORDER = 7   /* device self-check: same-address shared atomics of
+                                 one warp instruction did not return in lane order
+                                 (DESIGN.md 6); rerun with SHUF_RANK_MODE=match   */
 } shuf_status;
 
 /* Create a plan for shuffling n elements of elem_bytes bytes each with k
@@ -65,14 +68,27 @@ shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, uint32_t L, u
 /* Status of the last shuf_plan call on this thread. */
 shuf_status shuf_last_status(void);
 
-/* Bytes of device scratch shuf_run / shuf_segmented need for this plan:
- * one ping-pong buffer of n*elem_bytes plus O(k * n / chunk + n / S_fuse)
- * words of per-level metadata.  Writes *bytes. */
+/* Bytes of device scratch shuf_run needs for this plan: one ping-pong buffer
+ * of n*elem_bytes plus per-level metadata sized from the planned recursion
+ * (<= 1 % of n*elem_bytes for inputs of 256 MB and more, a few
+ * hundred KB at most below that).  The per-level tables are sized for the
+ * planned structure with a 6-sigma margin; a run whose level would exceed
+ * them (astronomically rare for random draws) latches SHUF_ERR_SCRATCH on
+ * the device -- read it with shuf_last_device_error.  Writes *bytes. */
 shuf_status shuf_scratch_bytes(shuf_plan_t p, uint64_t *bytes);
+
+/* Bytes of device scratch shuf_segmented needs for num_segments segments of
+ * this plan's n elements in total: the worst case of min(num_segments,
+ * n / (S_fuse + 1) + 1) segments longer than the fused size at every level
+ * (segment lengths are device data, unknown at plan time). */
+shuf_status shuf_scratch_bytes_segmented(shuf_plan_t p, uint64_t num_segments, uint64_t *bytes);
 
 /* Shuffle ptr[0..n) in place (result in ptr) using `scratch` (device, at
  * least shuf_scratch_bytes).  Stream-ordered, no host synchronisation, no
- * allocation.  The permutation is DESIGN.md D6 with K = seed. */
+ * allocation.  The permutation is DESIGN.md D6 with K = seed.  Errors the
+ * device detects after the call returned (SHUF_ERR_DEPTH, SHUF_ERR_SCRATCH;
+ * the output is then incomplete) are only reported by shuf_last_device_error:
+ * callers MUST check it after synchronising before using the result. */
 shuf_status shuf_run(shuf_plan_t p, void *ptr, void *scratch, uint64_t scratch_bytes, void *stream);
 
 /* Segmented batch shuffle (D7): segment s = ptr[off[s] .. off[s+1])
@@ -80,7 +96,8 @@ shuf_status shuf_run(shuf_plan_t p, void *ptr, void *scratch, uint64_t scratch_b
  * and segment-relative positions.  d_offsets: DEVICE array of num_segments+1
  * ascending uint64, d_offsets[0] = 0, d_offsets[num_segments] = n (the plan's
  * n); empty segments allowed.  The offsets are not validated on the device
- * beyond the plan's bounds. */
+ * beyond the plan's bounds.  scratch: at least shuf_scratch_bytes_segmented
+ * (p, num_segments) bytes.  Device errors as for shuf_run. */
 shuf_status shuf_segmented(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, uint64_t num_segments,
                            void *scratch, uint64_t scratch_bytes, void *stream);
 

@@ -28,7 +28,7 @@ lib_path = os.path.join(_HERE, "libshuf.so")
 _lib = None
 
 STATUS = {0: "SHUF_OK", 1: "SHUF_ERR_INVALID_ARG", 2: "SHUF_ERR_UNSUPPORTED", 3: "SHUF_ERR_ALIGNMENT",
-          4: "SHUF_ERR_SCRATCH", 5: "SHUF_ERR_DEPTH", 6: "SHUF_ERR_CUDA"}
+          4: "SHUF_ERR_SCRATCH", 5: "SHUF_ERR_DEPTH", 6: "SHUF_ERR_CUDA", 7: "SHUF_ERR_RANK_ORDER"}
 
 # every symbol include/shuf.h declares
 EXPORTED_SYMBOLS = [
@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
     "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks", "shuf_aux_bytes_inplace", "shuf_run_inplace",
-    "shuf_debug_inplace_levels",
+    "shuf_debug_inplace_levels", "shuf_scratch_bytes_segmented",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish", "leaf"]
 
@@ -64,6 +64,8 @@ def lib():
         L.shuf_last_status.restype = i32
         L.shuf_scratch_bytes.argtypes = [vp, ctypes.POINTER(u64)]
         L.shuf_scratch_bytes.restype = i32
+        L.shuf_scratch_bytes_segmented.argtypes = [vp, u64, ctypes.POINTER(u64)]
+        L.shuf_scratch_bytes_segmented.restype = i32
         L.shuf_run.argtypes = [vp, vp, vp, u64, vp]
         L.shuf_run.restype = i32
         L.shuf_segmented.argtypes = [vp, vp, vp, u64, vp, u64, vp]
@@ -122,6 +124,9 @@ class Plan:
     def scratch_bytes(self) -> int:
         return shuf_scratch_bytes(self)
 
+    def scratch_bytes_segmented(self, num_segments: int) -> int:
+        return shuf_scratch_bytes_segmented(self, num_segments)
+
     @property
     def planned_levels(self) -> int:
         return shuf_planned_levels(self)
@@ -155,6 +160,13 @@ def shuf_plan(n: int, elem_bytes: int, k: int, L: int, seed: int) -> Plan:
 def shuf_scratch_bytes(plan: Plan) -> int:
     b = ctypes.c_uint64(0)
     _check(lib().shuf_scratch_bytes(plan.handle, ctypes.byref(b)), "shuf_scratch_bytes", plan)
+    return int(b.value)
+
+
+def shuf_scratch_bytes_segmented(plan: Plan, num_segments: int) -> int:
+    b = ctypes.c_uint64(0)
+    _check(lib().shuf_scratch_bytes_segmented(plan.handle, num_segments, ctypes.byref(b)),
+           "shuf_scratch_bytes_segmented", plan)
     return int(b.value)
 
 
@@ -308,7 +320,10 @@ def segmented_shuffle(x, offsets, k: int, L: int, seed: int, elem_bytes: int | N
     n = x.shape[0]
     eb = elem_bytes or (x.numel() * x.element_size() // max(1, n))
     plan = shuf_plan(n, eb, k, L, seed)
-    shuf_segmented(plan, x, offsets, _scratch_for(plan, x.device), stream)
+    import torch
+    scratch = torch.empty(max(1, shuf_scratch_bytes_segmented(plan, offsets.numel() - 1)), dtype=torch.uint8,
+                          device=x.device)
+    shuf_segmented(plan, x, offsets, scratch, stream)
     err = shuf_last_device_error(plan, stream)
     if err:
         raise ShufError(err, "shuf_segmented (device)")

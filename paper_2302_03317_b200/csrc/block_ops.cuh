@@ -36,6 +36,19 @@ __device__ __forceinline__ uint32_t warp_inclusive_sum(uint32_t v) {
     return v;
 }
 
+// Self-check of the ordered-atomic ranking (see the top of this file): the
+// lanes of one warp instruction that share a bucket must have received
+// consecutive slots in lane order.  One __match_any_sync per call (slow, ~60
+// SM-cycles), so callers sample it -- one round per tile / item.  A violation
+// latches SHUF_ERR_RANK_ORDER (7) in *err: the output is then not D6's.
+__device__ __forceinline__ void check_rank_order(uint32_t b, bool valid, uint32_t slot, uint32_t* err) {
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu);
+    const uint32_t lower = peers & lanemask_lt();
+    const int src = lower ? 31 - __clz(lower) : (int)(threadIdx.x & 31u);
+    const uint32_t prev = __shfl_sync(0xFFFFFFFFu, slot, src);
+    if (valid && lower && prev + 1u != slot) atomicCAS(err, 0u, 7u);
+}
+
 // Exclusive scan over one value per thread; returns the thread's exclusive
 // prefix, *total gets the block total.  wsum: shared scratch of NT/32+1 words.
 template <int NT>

@@ -507,7 +507,8 @@ __device__ __forceinline__ uint32_t s_scan(const RunParams& rp, const XView<EB>&
 // holds its elements in registers across a group barrier, then each takes
 // its slot with one ordered shared atomic (warp rounds in position order).
 template <int EB, bool NARROW, bool ORD>
-__device__ __forceinline__ void s_place(const XView<EB>& V, const XItem& it, unsigned char* base, uint32_t w) {
+__device__ __forceinline__ void s_place(const XView<EB>& V, const XItem& it, unsigned char* base, uint32_t w,
+                                        uint32_t* err) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
     constexpr uint32_t R = XCfg<EB>::R;
@@ -549,6 +550,7 @@ __device__ __forceinline__ void s_place(const XView<EB>& V, const XItem& it, uns
         } else {
             slot = warp_rank(Tw, b, valid, false);
         }
+        if (ORD && r == 0 && w == 0) check_rank_order(b, valid, slot, err);
         if (valid) el[slot] = v[r];
     }
 }
@@ -621,11 +623,12 @@ __device__ __forceinline__ void run_fast(const RunParams& rp, const XSrc& xs) {
                 defer = s_scan<EB, NARROW>(rp, V, V.bst(ds), V.perm(ds), it.start, it.len, sid);
                 if (dbg) rp.hdr->clk[ctl->dbg_s * 6 + 1] = clock64();
                 mbar_wait(&ctl->full[bi], (t >> 1) & 1u);  // the item's data
-                if (!defer) s_place<EB, NARROW, ORD>(V, it, item_base<EB>(V.buf(bi), it.start), w);
+                if (!defer) s_place<EB, NARROW, ORD>(V, it, item_base<EB>(V.buf(bi), it.start), w, &rp.hdr->error);
                 else if (sid == 0) rp.flags[it.child] = 1;  // the general kernel takes it
             } else {
                 mbar_wait(&ctl->full[bi], (t >> 1) & 1u);
             }
+            fence_proxy_async();  // placement writes, before C's bulk store of a finished item
             bar_group(kBarS, XSN);
             if (sid == 0) {
                 ctl->defer[ds] = defer;
@@ -658,6 +661,7 @@ __device__ __forceinline__ void run_fast(const RunParams& rp, const XSrc& xs) {
                     }
                 }
             }
+            fence_proxy_async();  // every writer of the buffer orders its writes before C's bulk store
             bar_group(kBarF, XF);
             if (tid == 0) {
                 if (dbg) rp.hdr->clk[ctl->dbg_f++ * 6 + 4] = clock64();

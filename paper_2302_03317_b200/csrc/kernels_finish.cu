@@ -140,6 +140,8 @@ __device__ __forceinline__ void item_load(const Item& it, const unsigned char* s
 template <int EB>
 __device__ __forceinline__ void item_store(const Item& it, unsigned char* dst, const unsigned char* buf) {
     const uint32_t tid = threadIdx.x;
+    fence_proxy_async();  // every thread that wrote buf orders its writes before the bulk store
+    __syncthreads();
     const uint64_t x0 = it.start * EB, x1 = (it.start + it.len) * EB;
     const uint64_t fl = x0 & ~15ull;
     const uint64_t A = (x0 + 15) & ~15ull, B = x1 & ~15ull;

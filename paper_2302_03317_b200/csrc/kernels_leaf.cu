@@ -276,10 +276,12 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
                 fy_leaf<EB>(lb + (x0 & 15u), 0u, (uint32_t)len, start - origin, make_key(key));
                 fyn += len;
             }
-            // ---- store: aligned body by one bulk copy, ends by words
+            // ---- store: aligned body by one bulk copy, ends by words; every lane
+            //      that wrote the slot orders its writes before the bulk store
+            fence_proxy_async();
+            __syncwarp();
             if (inb) {
                 if (body) {
-                    fence_proxy_async();
                     bulk_s2g(rp.buf0 + A, lb + (A - (x0 & ~15ull)), body);
                     bulk_commit();
                 }

@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelPara
                 } else {
                     slot = warp_rank(Tw, b, valid, false);
                 }
+                if (ORD && r == 0 && warp == 0) check_rank_order(b, valid, slot, &rp.hdr->error);
                 if (valid) {
                     el[slot] = v[r];
                     slotb[slot] = (D)b;
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelPara
         // a segment of <= 2^32 elements: every destination minus the segment
         // start fits 32 bits, so delta is kept modulo 2^32 (half the lookup
         // bytes in the copy-out); longer segments keep 64-bit deltas
-        const bool wide = (sg.len >> 32) != 0;
+        const bool wide = (sg.len >> 32) != 0 || (rp.dbg & 64u);  // SHUF_DBG=64: test hook forcing the 64-bit path
         for (uint32_t b = tid; b < k; b += kSW * 32) {
             if (wide) delta64[b] = running[b] - bst[b];
             else delta[b] = (uint32_t)(running[b] - sg.start) - bst[b];

@@ -30,7 +30,8 @@ struct shuf_plan_s {
     uint32_t eb, k, L;
     uint64_t seed;
     uint32_t S_fuse, chunk, levels, fin_nbuf;
-    ScratchLayout lay;
+    int defer_planned;  // SHUF_DEFER=1 at plan time: item records are laid out
+    ScratchLayout lay;  // shuf_run's layout (one level-0 segment)
     IpAuxLayout ipl;
     // device setup (lazily, first run)
     bool dev_ready;
@@ -92,13 +93,66 @@ static uint32_t plan_levels(uint64_t n, uint32_t k, uint32_t S_fuse) {
     return g + 1 > kMaxLevels ? kMaxLevels : g + 1;
 }
 
-static void compute_layout(shuf_plan_s* p) {
-    ScratchLayout& l = p->lay;
+// Upper bounds on the segments and chunks of every planned level (DESIGN.md
+// 5).  A single shuffle starts from one segment; level l+1's segments are
+// the children of level l's longer than S_fuse.  Each child of a parent of
+// mean size m is Binomial(m, 1/k): with p = P(child > S_fuse) (normal
+// approximation) the bound is E + 6 sqrt(E) + 4 for E = N p, N the number
+// of children, capped by N and by n / (S_fuse + 1).  Segmented mode starts
+// from up to segs0 user segments of unknown lengths, so every level takes the
+// worst case min(N, n / (S_fuse + 1) + 1).  A level beyond its bound latches
+// SHUF_ERR_SCRATCH (k_plan / k_init_segmented).
+static void level_caps(uint64_t n, uint32_t k, uint32_t S, uint64_t C, uint32_t levels, uint64_t segs0,
+                       bool segmented, uint64_t* segcap, uint64_t* chunkcap) {
+    const double worst = (double)(n / ((uint64_t)S + 1) + 1);
+    double cnt = (double)segs0, mean = segs0 ? (double)n / (double)segs0 : 0.0;
+    for (uint32_t l = 0; l < levels; ++l) {
+        double segs, elems;
+        if (l == 0) {
+            segs = cnt;
+            elems = (double)n;
+        } else {
+            const double N = cnt * k;
+            if (segmented) {
+                segs = N < worst ? N : worst;
+                elems = (double)n;
+            } else {
+                const double mu = mean / k, sd = std::sqrt(mean * (1.0 / k) * (1.0 - 1.0 / k)) + 1e-9;
+                const double z = ((double)S + 0.5 - mu) / sd;
+                const double pr = 0.5 * std::erfc(z / std::sqrt(2.0));
+                const double E = N * pr;
+                segs = std::ceil(E + 6.0 * std::sqrt(E) + 4.0);
+                if (segs > N) segs = N;
+                if (segs > worst) segs = worst;
+                const double big = mu + 6.0 * sd + 32.0;
+                elems = segs * (big > S + 1.0 ? big : S + 1.0);
+                if (elems > (double)n) elems = (double)n;
+                mean = mu > S + 1.0 ? mu : S + 1.0;
+            }
+        }
+        if (segs < 1) segs = 1;
+        cnt = segs;
+        segcap[l] = (uint64_t)segs;
+        chunkcap[l] = (uint64_t)(elems / (double)C) + (uint64_t)segs + 1;
+    }
+}
+
+// Scratch layout for up to segs0 level-0 segments (1 for shuf_run,
+// min(num_segments, n / (S_fuse + 1) + 1) for shuf_segmented).
+static ScratchLayout compute_layout(const shuf_plan_s* p, uint64_t segs0, bool segmented) {
+    ScratchLayout l{};
     const uint64_t n = p->n;
-    l.max_segs = n / ((uint64_t)p->S_fuse + 1) + 1;
-    l.max_chunks = n / p->chunk + l.max_segs + 1;
-    l.max_entries = l.max_chunks * p->k;
-    l.max_tiles = (l.max_entries + kScanTile - 1) / kScanTile + 1;
+    std::vector<uint64_t> sc(p->levels + 1, 0), cc(p->levels + 1, 0);
+    if (p->levels) level_caps(n, p->k, p->S_fuse, p->chunk, p->levels, segs0, segmented, sc.data(), cc.data());
+    for (int s = 0; s < 2; ++s) {
+        l.seg_cap[s] = l.chunk_cap[s] = 1;
+        for (uint32_t lv = (uint32_t)s; lv < p->levels; lv += 2) {
+            if (sc[lv] > l.seg_cap[s]) l.seg_cap[s] = sc[lv];
+            if (cc[lv] > l.chunk_cap[s]) l.chunk_cap[s] = cc[lv];
+        }
+        l.entry_cap[s] = l.chunk_cap[s] * p->k;
+        l.tile_cap[s] = (l.entry_cap[s] + kScanTile - 1) / kScanTile + 1;
+    }
     uint64_t off = 0;
     l.pingpong = off;
     off = align_up(off + n * p->eb + 16, 256);
@@ -106,25 +160,28 @@ static void compute_layout(shuf_plan_s* p) {
     off = align_up(off + sizeof(Header), 256);
     for (int s = 0; s < 2; ++s) {
         l.segs[s] = off;
-        off = align_up(off + l.max_segs * sizeof(SegDesc), 256);
+        off = align_up(off + l.seg_cap[s] * sizeof(SegDesc), 256);
         l.chunks[s] = off;
-        off = align_up(off + l.max_chunks * sizeof(ChunkDesc), 256);
+        off = align_up(off + l.chunk_cap[s] * sizeof(ChunkDesc), 256);
         l.counts[s] = off;
-        off = align_up(off + l.max_entries * 4, 256);
+        off = align_up(off + l.entry_cap[s] * 4, 256);
         l.prefix[s] = off;
-        off = align_up(off + l.max_entries * 8, 256);
+        off = align_up(off + l.entry_cap[s] * 8, 256);
         l.status[s] = off;
-        off = align_up(off + l.max_tiles * 8, 256);
+        off = align_up(off + l.tile_cap[s] * 8, 256);
     }
+    const uint64_t maxseg = l.seg_cap[0] > l.seg_cap[1] ? l.seg_cap[0] : l.seg_cap[1];
     l.flags = off;
-    off = align_up(off + l.max_segs * p->k, 256);
-    l.max_items = n / ((uint64_t)p->L + 1) + 1;
+    off = align_up(off + maxseg * p->k, 256);
+    l.max_items = p->defer_planned ? n / ((uint64_t)p->L + 1) + 1 : 0;
     l.items = off;
     off = align_up(off + l.max_items * item_rec_stride(p->k), 256);
     l.max_fused = n / ((uint64_t)p->L + 1) + 1;
     l.fused = off;
     off = align_up(off + l.max_fused * 4, 256);
     l.total = off;
+    l.meta = l.total - (n * p->eb);
+    return l;
 }
 
 // In-place aux: batches of <= cap stripes / segments; stripes of Z elements
@@ -208,12 +265,22 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     p->S_fuse = S;
     p->fin_nbuf = nbuf;
     const uint32_t T = kScatterTileBytes / elem_bytes;  // scatter tile (kernels_scatter.cu SCfg)
-    uint64_t C = (n + 16383) / 16384;
+    // chunks per level: at most 4096 (balanced over the persistent grid), and
+    // few enough that a level's count + prefix tables (12 B per (bucket,
+    // chunk)) stay within ~0.5 % of the data each
+    uint64_t target = (n * (uint64_t)elem_bytes) / (2400ull * k);
+    if (target < 1) target = 1;
+    if (target > 4096) target = 4096;
+    uint64_t C = (n + target - 1) / target;
     C = align_up(C < T ? T : C, T);
     if (C > 0x40000000ull) C = 0x40000000ull;
     p->chunk = (uint32_t)C;
     p->levels = plan_levels(n, k, S);
-    compute_layout(p);
+    {
+        const char* df = std::getenv("SHUF_DEFER");
+        p->defer_planned = (df && df[0] == '1') ? 1 : 0;
+    }
+    p->lay = compute_layout(p, n > S ? 1 : 0, false);
     compute_ip_layout(p);
     return p;
 }
@@ -299,7 +366,7 @@ static cudaError_t device_setup(shuf_plan_s* p) {
         // SHUF_DEFER=1: fused items whose children are all leaves leave them to the leaf kernel
         // (one more HBM round trip; measured slower on HOT)
         const char* df = std::getenv("SHUF_DEFER");
-        p->defer = (p->leafk && df && df[0] == '1') ? 1 : 0;
+        p->defer = (p->leafk && p->defer_planned && df && df[0] == '1') ? 1 : 0;
     }
     // persistent grids: SM count x resident CTAs per SM
     int oh = 1, os = 1, osc = 1, of = 1, ol = 1;
@@ -318,8 +385,11 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     return cudaSuccess;
 }
 
-static LevelParams level_params(const shuf_plan_s* p, unsigned char* sc, unsigned char* buf0, uint32_t level) {
-    const ScratchLayout& l = p->lay;
+// Level l's tables (slot l & 1) and the next level's (slot ^ 1).  max_segs /
+// max_chunks bound the slot a kernel WRITES: the next level's for k_plan,
+// level 0's own for the init kernels (init = true).
+static LevelParams level_params(const ScratchLayout& l, unsigned char* sc, unsigned char* buf0, uint32_t level,
+                                bool init = false) {
     Header* hdr = reinterpret_cast<Header*>(sc + l.header);
     const int s = (int)(level & 1u), t = s ^ 1;
     LevelParams lp;
@@ -334,19 +404,33 @@ static LevelParams level_params(const shuf_plan_s* p, unsigned char* sc, unsigne
     lp.nsegs = reinterpret_cast<SegDesc*>(sc + l.segs[t]);
     lp.nchunks = reinterpret_cast<ChunkDesc*>(sc + l.chunks[t]);
     lp.nctr = &hdr->lv[t];
-    lp.max_segs = l.max_segs;
-    lp.max_chunks = l.max_chunks;
+    lp.max_segs = init ? l.seg_cap[s] : l.seg_cap[t];
+    lp.max_chunks = init ? l.chunk_cap[s] : l.chunk_cap[t];
     unsigned char* buf1 = sc + l.pingpong;
     lp.src = (level & 1u) ? buf1 : buf0;
     lp.dst = (level & 1u) ? buf0 : buf1;
     return lp;
 }
 
-static shuf_status check_run_args(shuf_plan_s* p, void* ptr, void* scratch, uint64_t scratch_bytes) {
+static shuf_status check_run_args(shuf_plan_s* p, void* ptr, void* scratch, uint64_t scratch_bytes,
+                                  uint64_t need = ~0ull) {
     if (!p) return SHUF_ERR_INVALID_ARG;
     if (p->n > 1 && (!ptr || !scratch)) return SHUF_ERR_INVALID_ARG;
     if (((uintptr_t)ptr & 15u) || ((uintptr_t)scratch & 15u)) return SHUF_ERR_ALIGNMENT;
-    if (p->n > 1 && scratch_bytes < p->lay.total) return SHUF_ERR_SCRATCH;
+    if (p->n > 1 && scratch_bytes < (need == ~0ull ? p->lay.total : need)) return SHUF_ERR_SCRATCH;
+    return SHUF_OK;
+}
+
+// Layout of a segmented run: up to min(num_segments, n / (S_fuse + 1) + 1)
+// level-0 segments longer than S_fuse, worst case at every level.
+static uint64_t seg0_bound(const shuf_plan_s* p, uint64_t num_segments) {
+    const uint64_t w = p->n / ((uint64_t)p->S_fuse + 1) + 1;
+    return num_segments < w ? num_segments : w;
+}
+
+extern "C" shuf_status shuf_scratch_bytes_segmented(shuf_plan_t p, uint64_t num_segments, uint64_t* bytes) {
+    if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    *bytes = compute_layout(p, seg0_bound(p, num_segments), true).total;
     return SHUF_OK;
 }
 
@@ -384,11 +468,12 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     if (e) return cuda_fail(p, e);
     unsigned char* sc = static_cast<unsigned char*>(scratch);
     unsigned char* buf0 = static_cast<unsigned char*>(ptr);
-    Header* hdr = reinterpret_cast<Header*>(sc + p->lay.header);
+    const ScratchLayout lay = d_offsets ? compute_layout(p, seg0_bound(p, nsegs), true) : p->lay;
+    Header* hdr = reinterpret_cast<Header*>(sc + lay.header);
     p->last_hdr = hdr;
     RunParams rp;
     rp.buf0 = buf0;
-    rp.buf1 = sc + p->lay.pingpong;
+    rp.buf1 = sc + lay.pingpong;
     rp.hdr = hdr;
     rp.n = p->n;
     rp.eb = p->eb;
@@ -406,17 +491,17 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     rp.fast = (uint32_t)p->fast;
     rp.leafk = (uint32_t)p->leafk;
     rp.defer = (uint32_t)p->defer;
-    rp.items = sc + p->lay.items;
-    rp.fused = reinterpret_cast<uint32_t*>(sc + p->lay.fused);
-    rp.max_fused = p->leafk ? p->lay.max_fused : 0;  // the list holds children > L only
+    rp.items = sc + lay.items;
+    rp.fused = reinterpret_cast<uint32_t*>(sc + lay.fused);
+    rp.max_fused = p->leafk ? lay.max_fused : 0;  // the list holds children > L only
     {
         const char* dbg = std::getenv("SHUF_DBG");
         rp.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
     }
-    rp.flags = sc + p->lay.flags;
+    rp.flags = sc + lay.flags;
     uint64_t launches = 0;
     if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
-    const LevelParams lp0 = level_params(p, sc, buf0, 0);
+    const LevelParams lp0 = level_params(lay, sc, buf0, 0, true);
     if (d_offsets) {
         LAUNCH(SHUF_K_INIT, launch_init_segmented(rp, lp0, d_offsets, nsegs, st, p->grid_small));
         LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, d_offsets, nsegs, st, p->grid_finish));
@@ -430,7 +515,7 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     }
     const uint32_t G = p->levels < max_levels ? p->levels : max_levels;
     for (uint32_t lv = 0; lv < G; ++lv) {
-        const LevelParams lp = level_params(p, sc, buf0, lv);
+        const LevelParams lp = level_params(lay, sc, buf0, lv);
         LAUNCH(SHUF_K_HIST, launch_hist(rp, lp, st, p->grid_hist));
         LAUNCH(SHUF_K_SCAN, launch_scan(rp, lp, st, p->grid_scan));
         LAUNCH(SHUF_K_PLAN, launch_plan(rp, lp, st, p->grid_small));
@@ -629,7 +714,8 @@ extern "C" shuf_status shuf_debug_run_levels(shuf_plan_t p, void* ptr, void* scr
 
 extern "C" shuf_status shuf_segmented(shuf_plan_t p, void* ptr, const uint64_t* d_offsets, uint64_t num_segments,
                                       void* scratch, uint64_t scratch_bytes, void* stream) {
-    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes,
+                                   p ? compute_layout(p, seg0_bound(p, num_segments), true).total : 0);
     if (s) return s;
     if (!d_offsets) return SHUF_ERR_INVALID_ARG;
     if ((uintptr_t)d_offsets & 7u) return SHUF_ERR_ALIGNMENT;
@@ -643,7 +729,8 @@ extern "C" shuf_status shuf_segmented(shuf_plan_t p, void* ptr, const uint64_t* 
 extern "C" shuf_status shuf_profile_run(shuf_plan_t p, void* ptr, const uint64_t* d_offsets, uint64_t num_segments,
                                         void* scratch, uint64_t scratch_bytes, void* stream, float* ms_by_class,
                                         uint32_t* launches_by_class) {
-    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes,
+                                   p && d_offsets ? compute_layout(p, seg0_bound(p, num_segments), true).total : ~0ull);
     if (s) return s;
     if (!ms_by_class || !launches_by_class) return SHUF_ERR_INVALID_ARG;
     for (int c = 0; c < SHUF_K_CLASSES; ++c) {
@@ -727,6 +814,7 @@ extern "C" const char* shuf_status_string(shuf_status s) {
     case SHUF_ERR_SCRATCH: return "scratch buffer too small";
     case SHUF_ERR_DEPTH: return "more scatter levels than planned";
     case SHUF_ERR_CUDA: return "CUDA error";
+    case SHUF_ERR_RANK_ORDER: return "ordered-atomic ranking self-check failed (use SHUF_RANK_MODE=match)";
     }
     return "unknown status";
 }

@@ -64,7 +64,11 @@ struct Header {
     long long sclk[256];                  // phase timestamps of CTA 0 of the level-0 HBM scatter
 };
 
-// Byte offsets of every region inside the caller's scratch buffer.
+// Byte offsets of every region inside the caller's scratch buffer.  The
+// per-level tables are sized from the planned structure (shuf_api.cu
+// level_caps): slot s holds the levels l with l & 1 == s, so its capacity is
+// the largest bound among them.  A level that would overflow its slot latches
+// SHUF_ERR_SCRATCH on the device.
 struct ScratchLayout {
     uint64_t pingpong;  // n * eb
     uint64_t header;
@@ -74,12 +78,13 @@ struct ScratchLayout {
     uint64_t prefix[2];  // u64 per (bucket, chunk)
     uint64_t status[2];  // u64 per scan tile
     uint64_t flags;      // u8 per child of a level: 1 = finished by the general finish kernel
-    uint64_t items;      // item records (item_rec_stride bytes each), max_items of them
+    uint64_t items;      // item records (item_rec_stride bytes each), max_items of them (SHUF_DEFER=1 only)
     uint64_t max_items;
     uint64_t fused;      // u32 child indices of the current level that the finish kernels take
     uint64_t max_fused;
     uint64_t total;
-    uint64_t max_segs, max_chunks, max_entries, max_tiles;
+    uint64_t seg_cap[2], chunk_cap[2], entry_cap[2], tile_cap[2];
+    uint64_t meta;       // total - pingpong bytes: the metadata
 };
 
 // Everything a kernel needs about the run (passed by value).

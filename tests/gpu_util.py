@@ -41,7 +41,7 @@ def gpu_segmented(a: np.ndarray, offsets: np.ndarray, k: int, L: int, seed: int)
     x = to_dev(a)
     off = torch.from_numpy(np.asarray(offsets, dtype=np.uint64).view(np.int64)).cuda()
     plan = shuf.shuf_plan(a.shape[0], elem_bytes(a), k, L, seed)
-    scratch = torch.empty(max(1, plan.scratch_bytes), dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(max(1, plan.scratch_bytes_segmented(off.numel() - 1)), dtype=torch.uint8, device="cuda")
     shuf.shuf_segmented(plan, x, off, scratch)
     assert shuf.shuf_last_device_error(plan) == 0
     return to_host(x, a)

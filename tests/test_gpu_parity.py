@@ -55,7 +55,9 @@ CASES = [
     (300_001, 1000, 50, 7, 4),                                          # k with rejections
     (200_000, 2, 1, 8, 4),                                              # deepest recursion
     (123_457, 64, 2048, 9, 8), (99_991, 1024, 2048, 10, 16),            # element sizes
-    (3_000_000, 256, 4096, 11, 4),                                      # 2 global levels
+    (3_000_000, 256, 4096, 11, 4),                                      # 1 HBM level (+1 planned spare), fused
+    (1 << 25, 64, 300, 21, 4),                                          # HOT's shape: 2 HBM levels, then the
+    (1 << 26, 256, 64, 22, 4),                                          #  pipelined finish, then FY leaves
     (2_000_000, 256, 1000, 12, 8), (1_000_000, 256, 500, 13, 16),       # fused items of 8/16-byte elements
     (1_500_000, 1024, 600, 14, 16),                                     # k = 1024: several leaves per FY thread
 ]
@@ -158,6 +160,38 @@ def test_documented_match_rank_path_bit_exact():
         "print('ok')\n" % root)
     env = dict(os.environ, SHUF_RANK_MODE="match")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+_WIDE_CASES = (
+    "import sys; sys.path.insert(0, %r)\n"
+    "import numpy as np, oracle, synth\n"
+    "from tests.gpu_util import gpu_shuffle, gpu_segmented\n"
+    "for n, k, L, seed in [(3_000_000, 256, 4096, 11), (1 << 25, 64, 300, 21), (777_777, 7, 300, 6),\n"
+    "                      (300_001, 1000, 50, 7), (200_000, 2, 1, 8)]:\n"
+    "    a = np.arange(n, dtype=np.uint32)\n"
+    "    assert (gpu_shuffle(a, k, L, seed) == oracle.shuffle(a, k, L, seed)).all(), (n, k, L, seed)\n"
+    "b = synth.splitmix64_stream_np(3, 0, 2_000_000)\n"
+    "assert (gpu_shuffle(b, 256, 1000, 12) == oracle.shuffle(b, 256, 1000, 12)).all()\n"
+    "c = synth.make_input_np(synth.WORKLOADS['c4'], n=1_500_000)\n"
+    "assert (gpu_shuffle(c, 1024, 600, 14) == oracle.shuffle(c, 1024, 600, 14)).all()\n"
+    "off = np.array([0, 0, 1, 3000, 300000, 309001, 900000], dtype=np.uint64)\n"
+    "d = np.arange(int(off[-1]), dtype=np.uint32)\n"
+    "assert (gpu_segmented(d, off, 64, 4096, 5) == oracle.segmented(d, off, 64, 4096, 5)).all()\n"
+    "print('ok')\n")
+
+
+def test_wide_run_offsets_bit_exact():
+    """The HBM scatter keeps 64-bit run offsets for segments longer than 2^32
+    elements (only config 4's level 0 at full size); SHUF_DBG=64 forces that
+    branch for every segment so it is compared with the oracle bit for bit
+    at small n (every element size, HBM levels, segmented mode)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _WIDE_CASES % root], env=dict(os.environ, SHUF_DBG="64"),
+                       capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 

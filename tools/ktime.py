@@ -24,7 +24,8 @@ else:
     n = w.n
     x = synth.make_input_torch(w, dev)
 plan = shuf.shuf_plan(n, w.elem_bytes, w.k, w.L, w.seed)
-scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
+scratch = torch.empty(plan.scratch_bytes if d_off is None else plan.scratch_bytes_segmented(d_off.numel() - 1),
+                      dtype=torch.uint8, device=dev)
 
 
 INPLACE = "--inplace" in sys.argv

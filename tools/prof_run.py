@@ -32,7 +32,8 @@ else:
     x = synth.make_input_torch(w, dev, n=a.n or None)
 n = x.shape[0]
 plan = shuf.shuf_plan(n, w.elem_bytes, w.k, w.L, w.seed)
-scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=dev)
+scratch = torch.empty(plan.scratch_bytes if d_off is None else plan.scratch_bytes_segmented(d_off.numel() - 1),
+                      dtype=torch.uint8, device=dev)
 for _ in range(a.reps):
     if d_off is None:
         shuf.shuf_run(plan, x, scratch)
