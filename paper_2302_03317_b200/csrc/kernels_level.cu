@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
     if (gtid() == 0) {
         lp.ctr->scan_ticket = 0;
         lp.ctr->nfuse = 0;
-        lp.nctr->nseg = 0;
-        lp.nctr->nchunk = 0;
+        // (the next level's segment counters are reset by k_scan: this kernel may
+        // run while the previous level's kernels still read that slot)
     }
     const uint32_t k = rp.k;
     const BucketParams bp = rp.bp;
@@ -166,6 +166,10 @@ __global__ void __launch_bounds__(kThreads) k_scan(RunParams rp, LevelParams lp)
     const uint64_t E = (uint64_t)lp.ctr->nchunk * rp.k;
     const uint64_t ntiles = (E + kScanTile - 1) / kScanTile;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (blockIdx.x == 0 && tid == 0) {  // the next level's list, filled by k_plan after this kernel
+        lp.nctr->nseg = 0;
+        lp.nctr->nchunk = 0;
+    }
     for (;;) {
         if (tid == 0) s_tile = atomicAdd(&lp.ctr->scan_ticket, 1u);
         __syncthreads();

@@ -5,24 +5,31 @@
 // A CTA owns chunks (contiguous runs of C elements of one segment; k_scan
 // gave each (segment, bucket, chunk) its destination) and walks each chunk
 // tile by tile in order, keeping per bucket the running destination of the
-// chunk's next element.  Per tile of T elements (double-buffered: the next
-// tile's bulk async copy, TMA engine, is in flight while this one is
-// processed):
-//   1. draws + counts: warp w owns a contiguous run of the tile's Philox
-//      groups (D4: 16 draws per call for power-of-two k <= 256), writes the
-//      draws to shared memory and counts its elements per bucket in its own
-//      table (unordered shared reductions);
-//   2. scan: bucket starts of the tile and per-warp slot bases;
-//   3. place: every thread reads its elements into registers, then writes
-//      each to its slot in the same buffer -- warp w walks its elements in
-//      rounds of 32 in position order and one ordered shared atomic on its
-//      own table returns the slot (stable; the documented __match_any_sync
-//      path when the probe in shuf_api.cu did not verify the order);
-//   4. copy-out: slot s of the tile goes to dst[delta[b] + s] (b = bucket of
-//      the slot, delta[b] = running[b] - tile start of run b): consecutive
-//      lanes write consecutive slots, i.e. whole runs, coalesced.
+// chunk's next element.  NW warps; warp w owns elements [w*R*32, (w+1)*R*32)
+// of a tile of T elements (R rounds of 32 consecutive elements, lane order =
+// position order).  Separate buffers for the raw tile (bulk async copy, TMA
+// engine) and the bucket-sorted tile, so no element is held in registers
+// across a barrier.  Per tile t, three CTA barriers:
+//
+//   B(t)   scan: (bucket, warp)-major exclusive prefix of the counts -> per-
+//          warp slot bases, tile bucket starts, run destinations delta
+//   C(t)   rank + place: each round reads 32 draws and 32 elements of the raw
+//          tile, takes every element's slot with one ordered shared atomic on
+//          the warp's table (whose entries the scan set to the warp's first
+//          slot per bucket) and stores element and bucket at that slot
+//   ---- barrier: raw tile consumed -> bulk load of tile t+1 into it
+//   D(t)   copy-out: slot x -> dst[delta[bucket(x)] + x]; consecutive lanes
+//          take consecutive slots, i.e. whole bucket runs (coalesced)
+//   A(t+1) draws + counts of the next tile (D4 Philox: positions only, no
+//          data): lane-owned Philox groups -> draw buffer, per-warp counts
+//   ---- barrier
+//
+// (plus the two barriers inside the scan).  Full tiles take an unrolled path
+// with compile-time offsets (every element valid); a chunk's last partial
+// tile takes the checked path.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "block_ops.cuh"
@@ -30,26 +37,30 @@
 
 namespace shuf {
 
-constexpr uint32_t kSW = 8;  // warps per CTA: 256 threads, 2 CTAs per SM (32 KiB tiles)
-
-template <int EB>
+// Tile geometry.  V selects an experimental variant (SHUF_SCV, u32 narrow only):
+// 0 = 32 KiB tiles x 16 warps (default), 1 = 32 KiB x 8 warps, 2 = 16 KiB x 8
+// warps, 3 = 16 KiB x 16 warps, 4 = 32 KiB x 4 warps, 5 = as 1 with packed u16
+// counters, 6 = 24 KiB x 8 warps.
+template <int EB, bool NARROW, int V = 0>
 struct SCfg {
-    static constexpr uint32_t T = kScatterTileBytes / EB;  // elements per tile (32 KiB)
+    static constexpr uint32_t TB = (V == 2 || V == 3) ? 16384u : (V == 6 ? 24576u : kScatterTileBytes);
+    static constexpr uint32_t T = TB / EB;  // elements per tile
+    static constexpr uint32_t NW = V == 4 ? 4u : ((!NARROW || V == 1 || V == 2 || V == 5 || V == 6) ? 8u : 16u);
+    static constexpr uint32_t NT = NW * 32u;
+    static constexpr uint32_t R = T / (NW * 32u);  // rounds per warp
+    static constexpr uint32_t sh = NARROW ? 4u : 3u;  // log2 draws per Philox group
+    static constexpr uint32_t dpg = 1u << sh;
+    static constexpr bool P16 = !NARROW || V == 5;    // counters as packed u16 pairs (else u32)
+    static constexpr int MINB = !NARROW ? 1 : (V == 2 ? 4 : (V == 4 || V == 6 ? 3 : 2));
 };
-
-// Draw storage of a tile: one 16-byte slot per Philox group (+1 for the
-// misaligned head), u8 draws for power-of-two k <= 256, u16 otherwise.
-template <int EB>
-__host__ __device__ inline uint32_t scatter_draw_bytes(bool narrow) {
-    return (SCfg<EB>::T / (narrow ? 16 : 8) + 2) * 16;
-}
 
 struct SLayout {
-    uint32_t buf0, buf1, draws, slotb, tab, bst, run, delta, wsum, bar, total;
+    uint32_t raw, sorted, draws, slotb, tab, bst, run, delta, wsum, bar, total;
 };
 
-template <int EB>
+template <int EB, bool NARROW, int V = 0>
 __host__ __device__ inline SLayout s_layout(uint32_t k) {
+    using C = SCfg<EB, NARROW, V>;
     SLayout L;
     uint32_t off = 0;
     auto take = [&off](uint32_t bytes) {
@@ -57,27 +68,50 @@ __host__ __device__ inline SLayout s_layout(uint32_t k) {
         off = (off + bytes + 15u) & ~15u;
         return at;
     };
-    L.buf0 = take(SCfg<EB>::T * EB + 16);
-    L.buf1 = take(SCfg<EB>::T * EB + 16);
-    const bool narrow = (k & (k - 1)) == 0 && k <= 256;
-    L.draws = take(scatter_draw_bytes<EB>(narrow));
-    L.slotb = take((narrow ? 1u : 2u) * SCfg<EB>::T);  // bucket of every slot (u8 / u16)
-    L.tab = take(kSW * (narrow ? k : (k + 1) / 2) * 4);  // u32 counters (narrow k) or packed u16 pairs
+    L.raw = take(C::T * EB + 16);
+    L.sorted = take(C::T * EB);
+    L.draws = take((C::T / C::dpg + 2) * 16);
+    L.slotb = take((NARROW ? 1u : 2u) * C::T);             // bucket of every slot (u8 / u16)
+    L.tab = take(C::NW * (C::P16 ? (k + 1) / 2 : k) * 4);  // u32 counters or packed u16 pairs
     L.bst = take((k + 1) * 4);
     L.run = take(k * 8);
     L.delta = take(k * 8);  // destination minus slot: u32 relative to the segment start (mod 2^32),
                             // u64 absolute for segments longer than 2^32 elements
-    L.wsum = take((kSW + 1) * 4);
+    L.wsum = take((C::NW + 1) * 4);
     L.bar = take(16);
     L.total = off;
     return L;
 }
 
+static bool is_narrow(uint32_t k) { return (k & (k - 1)) == 0 && k <= 256; }
+
+static int g_scv = -1;
+static int scv() {
+    if (g_scv < 0) {
+        const char* e = std::getenv("SHUF_SCV");
+        g_scv = e ? std::atoi(e) : 1;
+        if (g_scv < 0 || g_scv > 6) g_scv = 1;
+    }
+    return g_scv;
+}
+
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k) {
+    const bool nr = is_narrow(k);
+    if (eb == 4 && nr) {
+        switch (scv()) {
+        case 1: return s_layout<4, true, 1>(k).total;
+        case 2: return s_layout<4, true, 2>(k).total;
+        case 3: return s_layout<4, true, 3>(k).total;
+        case 4: return s_layout<4, true, 4>(k).total;
+        case 5: return s_layout<4, true, 5>(k).total;
+        case 6: return s_layout<4, true, 6>(k).total;
+        default: break;
+        }
+    }
     switch (eb) {
-    case 4: return s_layout<4>(k).total;
-    case 8: return s_layout<8>(k).total;
-    default: return s_layout<16>(k).total;
+    case 4: return nr ? s_layout<4, true>(k).total : s_layout<4, false>(k).total;
+    case 8: return nr ? s_layout<8, true>(k).total : s_layout<8, false>(k).total;
+    default: return nr ? s_layout<16, true>(k).total : s_layout<16, false>(k).total;
     }
 }
 
@@ -130,23 +164,136 @@ __device__ __forceinline__ void s_issue_load(uint64_t q0, uint32_t cnt, const un
             *reinterpret_cast<const uint32_t*>(src + tBeg + 4 * (tid - 64));
 }
 
-template <int EB, bool ORD, bool NARROW>
-__global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelParams lp) {
+// A: draws of the tile at problem positions [P0, P0+cnt) -> draw buffer
+// (16-byte group t holds the draws of positions ((P0 >> sh) + t) << sh ..),
+// and warp w's per-bucket counts of its element range (unordered shared
+// reductions on the warp's own table).
+template <int EB, bool NARROW, int V>
+__device__ __forceinline__ void s_draw_count(const BucketParams& bp, PhiloxKey key, uint32_t level, uint64_t P0,
+                                             uint32_t cnt, unsigned char* draws, uint32_t* Tw, uint32_t kw,
+                                             uint32_t warp, uint32_t lane) {
+    using C = SCfg<EB, NARROW, V>;
+    constexpr uint32_t sh = C::sh, dpg = C::dpg;
+    for (uint32_t i = lane; i < kw; i += 32) Tw[i] = 0;
+    __syncwarp();
+    const uint32_t doff = (uint32_t)(P0 & (dpg - 1));
+    const int32_t e_lo = (int32_t)(warp * C::R * 32u);
+    const int32_t e_hi = min(e_lo + (int32_t)(C::R * 32u), (int32_t)cnt);
+    if (e_hi <= e_lo) return;
+    // element e lies in group (e + doff) >> sh
+    const uint32_t t0 = (uint32_t)(e_lo + (int32_t)doff) >> sh;
+    const uint32_t t1 = (uint32_t)(e_hi - 1 + (int32_t)doff) >> sh;  // inclusive
+    const uint64_t g0 = P0 >> sh;
+    for (uint32_t t = t0 + lane; t <= t1; t += 32) {
+        const uint4 w4 = bucket_group_words(key, level, g0 + t);
+        const int32_t es = (int32_t)(t * dpg) - (int32_t)doff;  // element index of the group's lane 0
+        uint4 packed;
+        if (NARROW) {
+            const uint32_t msk = (0xFFu >> bp.shift) * 0x01010101u;
+            packed = make_uint4((w4.x >> bp.shift) & msk, (w4.y >> bp.shift) & msk, (w4.z >> bp.shift) & msk,
+                                (w4.w >> bp.shift) & msk);
+        } else {
+            const uint64_t pb = (g0 + t) << sh;
+            uint32_t bb[8];
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const int32_t e = es + (int32_t)j;
+                bb[j] = (e >= 0 && e < (int32_t)cnt) ? bucket_from_group(w4, j, key, level, pb + j, bp) : 0u;
+            }
+            packed = make_uint4(bb[0] | (bb[1] << 16), bb[2] | (bb[3] << 16), bb[4] | (bb[5] << 16),
+                                bb[6] | (bb[7] << 16));
+        }
+        // a group straddling two warp ranges is written by the warp it starts in
+        if (es >= e_lo || warp == 0) *reinterpret_cast<uint4*>(draws + (size_t)t * 16) = packed;
+        const uint32_t pw4[4] = {packed.x, packed.y, packed.z, packed.w};
+        if (es >= e_lo && es + (int32_t)dpg <= e_hi) {  // whole group in this warp's range
+#pragma unroll
+            for (uint32_t j = 0; j < dpg; ++j) {
+                const uint32_t b = NARROW ? __byte_perm(pw4[j >> 2], 0u, 0x4440u | (j & 3u))
+                                          : (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
+                if (C::P16) atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
+                else atomicAdd(&Tw[b], 1u);
+            }
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < dpg; ++j) {
+                const int32_t e = es + (int32_t)j;
+                if (e >= e_lo && e < e_hi) {
+                    const uint32_t b = NARROW ? (pw4[j >> 2] >> ((j & 3u) * 8u)) & 0xFFu
+                                              : (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
+                    if (C::P16) atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
+                    else atomicAdd(&Tw[b], 1u);
+                }
+            }
+        }
+    }
+}
+
+// C: rank + place of warp w's rounds.  FULL: cnt == T (no checks).
+template <int EB, bool NARROW, bool ORD, bool FULL, int V>
+__device__ __forceinline__ void s_place(const unsigned char* raw, uint64_t q0, const unsigned char* draws,
+                                        uint32_t doff, uint32_t cnt, unsigned char* sorted, unsigned char* slotb_,
+                                        uint32_t* Tw, uint32_t warp, uint32_t lane, uint32_t* err) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
-    constexpr uint32_t T = SCfg<EB>::T;
-    constexpr uint32_t sh = NARROW ? 4u : 3u, dpg = 1u << sh;
-    constexpr uint32_t R = (T / dpg / kSW + 1) * dpg / 32 + 1;  // rounds per warp (upper bound)
+    using C = SCfg<EB, NARROW, V>;
+    const uint32_t e0 = warp * C::R * 32u;
+    const E* el = reinterpret_cast<const E*>(raw + ((q0 * EB) & 15u)) + e0 + lane;
+    const D* dp = reinterpret_cast<const D*>(draws) + doff + e0 + lane;
+    E* so = reinterpret_cast<E*>(sorted);
+    D* sb = reinterpret_cast<D*>(slotb_);
+    const int32_t wrem = (int32_t)cnt - (int32_t)e0;  // elements of this warp's range in the tile
+#pragma unroll
+    for (uint32_t r = 0; r < C::R; ++r) {
+        if (!FULL && (int32_t)(r * 32u) >= wrem) break;  // warp-uniform
+        const bool valid = FULL || (int32_t)(r * 32u + lane) < wrem;
+        const uint32_t b = valid ? (uint32_t)dp[r * 32u] : 0u;
+        const E v = el[(FULL || valid) ? r * 32u : 0u];
+        uint32_t slot;
+        if (!C::P16) {
+            if (ORD) {
+                slot = atomicAdd(&Tw[b], valid ? 1u : 0u);
+            } else {
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu);
+                const uint32_t old = valid ? Tw[b] : 0u;
+                __syncwarp();
+                if (valid && (peers & lanemask_lt()) == 0) Tw[b] = old + (uint32_t)__popc(peers);
+                __syncwarp();
+                slot = old + __popc(peers & lanemask_lt());
+            }
+        } else if (ORD) {
+            const uint32_t shb = (b & 1u) << 4;
+            slot = (atomicAdd(&Tw[b >> 1], valid ? (1u << shb) : 0u) >> shb) & 0xFFFFu;
+        } else {
+            slot = warp_rank(Tw, b, valid, false);
+        }
+        if (ORD && r == 0 && warp == 0) check_rank_order(b, valid, slot, err);
+        if (valid) {
+            so[slot] = v;
+            sb[slot] = (D)b;
+        }
+    }
+}
+
+template <int EB, bool NARROW, bool ORD, int V = 0>
+__global__ void __launch_bounds__(SCfg<EB, NARROW, V>::NT, SCfg<EB, NARROW, V>::MINB)
+    k_scatter(RunParams rp, LevelParams lp) {
+    using E = typename ElemT<EB>::type;
+    using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
+    using C = SCfg<EB, NARROW, V>;
+    constexpr uint32_t T = C::T, NT = C::NT;
     extern __shared__ __align__(16) unsigned char sm[];
-    const uint32_t k = rp.k, kw = NARROW ? k : (k + 1) >> 1;  // table words per warp
-    const SLayout Ly = s_layout<EB>(k);
+    const uint32_t k = rp.k, kw = C::P16 ? (k + 1) >> 1 : k;  // table words per warp
+    const SLayout Ly = s_layout<EB, NARROW, V>(k);
+    unsigned char* raw = sm + Ly.raw;
+    unsigned char* sorted = sm + Ly.sorted;
     unsigned char* draws = sm + Ly.draws;
+    unsigned char* slotb = sm + Ly.slotb;
     uint32_t* tab = reinterpret_cast<uint32_t*>(sm + Ly.tab);
     uint32_t* bst = reinterpret_cast<uint32_t*>(sm + Ly.bst);
     uint64_t* running = reinterpret_cast<uint64_t*>(sm + Ly.run);
     uint32_t* delta = reinterpret_cast<uint32_t*>(sm + Ly.delta);
     uint64_t* delta64 = reinterpret_cast<uint64_t*>(sm + Ly.delta);
-    D* slotb = reinterpret_cast<D*>(sm + Ly.slotb);
     uint32_t* wsum = reinterpret_cast<uint32_t*>(sm + Ly.wsum);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + Ly.bar);
     const BucketParams bp = rp.bp;
@@ -156,26 +303,54 @@ __global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelPara
     if (blockIdx.x >= nchunk) return;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
     const unsigned char* __restrict__ src = lp.src;
     unsigned char* __restrict__ dstb = lp.dst;
-    uint32_t ph0 = 0, ph1 = 0;
+    uint32_t ph = 0;
     uint32_t* Tw = tab + warp * kw;
 
+    // ---- prologue: tile 0's load, draws + counts
     STile cur = s_first_tile(lp, rp, blockIdx.x, nchunk);
     uint32_t cnt = (uint32_t)min((uint64_t)T, cur.q1 - cur.q0);
-    s_issue_load<EB>(cur.q0, cnt, src, sm + Ly.buf0, &bar[0]);
     unsigned long long scattered = cur.q1 - cur.q0;
+    s_issue_load<EB>(cur.q0, cnt, src, raw, &bar[0]);
+    SegDesc sg = lp.segs[cur.seg];
+    s_draw_count<EB, NARROW, V>(bp, make_key(sg.key), lp.level, cur.q0 - sg.origin, cnt, draws, Tw, kw, warp, lane);
     bool new_chunk = true;
-    const bool dbgc = (rp.dbg & 1u) && blockIdx.x == 0 && tid == 0 && lp.level == 0;
-    for (uint32_t it = 0; cur.chunk < nchunk; ++it) {
-        const bool dbg = dbgc && it < 40;
-        if (dbg) rp.hdr->sclk[it * 6 + 0] = clock64();
-        // ---- next tile of this CTA's sequence -> the other buffer (free since
-        //      the previous iteration's copy-out)
+    __syncthreads();
+    for (;;) {
+        // ---- B: scan of the counts of tile `cur` -> slot bases, bucket starts, run destinations
+        if (new_chunk) {
+            const ChunkDesc ch = lp.chunks[cur.chunk];
+            const uint64_t base0 = lp.prefix[sg.cbase];
+            for (uint32_t b = tid; b < k; b += NT)
+                running[b] = sg.start + lp.prefix[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] - base0;
+        }
+        if (!C::P16) scan_counters32<NT>(tab, C::NW, k, bst, wsum);
+        else scan_counters<NT>(tab, C::NW, k, bst, wsum);
+        // a segment of <= 2^32 elements: every destination minus the segment
+        // start fits 32 bits, so delta is kept modulo 2^32 (half the lookup
+        // bytes in the copy-out); longer segments keep 64-bit deltas
+        const bool wide = (sg.len >> 32) != 0 || (rp.dbg & 64u);  // SHUF_DBG=64: test hook forcing the 64-bit path
+        for (uint32_t b = tid; b < k; b += NT) {
+            if (wide) delta64[b] = running[b] - bst[b];
+            else delta[b] = (uint32_t)(running[b] - sg.start) - bst[b];
+            running[b] += bst[b + 1] - bst[b];
+        }
+        // ---- C: rank + place (the tile's data must have landed)
+        mbar_wait(&bar[0], ph);
+        ph ^= 1u;
+        const uint32_t doff = (uint32_t)((cur.q0 - sg.origin) & (C::dpg - 1));
+        if (cnt == T)
+            s_place<EB, NARROW, ORD, true, V>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
+                                           &rp.hdr->error);
+        else
+            s_place<EB, NARROW, ORD, false, V>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
+                                            &rp.hdr->error);
+        __syncthreads();  // raw consumed; sorted, slotb and delta complete
+        // ---- next tile of this CTA's sequence: load it into the raw buffer
         STile nxt = cur;
         nxt.q0 = cur.q0 + cnt;
         const bool next_chunk = nxt.q0 >= cur.q1;
@@ -184,172 +359,37 @@ __global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelPara
             if (nxt.chunk < nchunk) scattered += nxt.q1 - nxt.q0;
         }
         const uint32_t ncnt = (uint32_t)min((uint64_t)T, nxt.q1 - nxt.q0);
-        unsigned char* buf = sm + ((it & 1u) ? Ly.buf1 : Ly.buf0);
-        if (nxt.chunk < nchunk)
-            s_issue_load<EB>(nxt.q0, ncnt, src, sm + ((it & 1u) ? Ly.buf0 : Ly.buf1), &bar[(it & 1u) ^ 1u]);
-        const SegDesc sg = lp.segs[cur.seg];
-        if (new_chunk) {
-            const ChunkDesc ch = lp.chunks[cur.chunk];
-            const uint64_t base0 = lp.prefix[sg.cbase];
-            for (uint32_t b = tid; b < k; b += kSW * 32)
-                running[b] = sg.start + lp.prefix[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] - base0;
-        }
-        // ---- 1. draws + per-warp counts
-        const uint64_t P0 = cur.q0 - sg.origin;
-        const uint64_t g0 = P0 >> sh;
-        const uint32_t doff = (uint32_t)(P0 & (dpg - 1));
-        const uint32_t ng = (uint32_t)(((P0 + cnt - 1) >> sh) - g0 + 1);
-        const uint32_t qg = (ng + kSW - 1) / kSW;
+        if (nxt.chunk < nchunk) s_issue_load<EB>(nxt.q0, ncnt, src, raw, &bar[0]);
+        // ---- D: copy-out of tile `cur`: slot x -> dst[delta[bucket(x)] + x]
         {
-            const PhiloxKey key = make_key(sg.key);
-            for (uint32_t i = lane; i < kw; i += 32) Tw[i] = 0;
-            __syncwarp();
-            const uint32_t t1 = min(ng, (warp + 1) * qg);
-            for (uint32_t t = warp * qg + lane; t < t1; t += 32) {
-                const uint64_t g = g0 + t;
-                const uint4 w4 = bucket_group_words(key, lp.level, g);
-                uint4 packed;
-                if (NARROW) {
-                    const uint32_t msk = (0xFFu >> bp.shift) * 0x01010101u;
-                    packed = make_uint4((w4.x >> bp.shift) & msk, (w4.y >> bp.shift) & msk, (w4.z >> bp.shift) & msk,
-                                        (w4.w >> bp.shift) & msk);
-                } else {
-                    const uint64_t pb = g << sh;
-                    uint32_t bb[8];
-#pragma unroll
-                    for (uint32_t j = 0; j < 8; ++j) {
-                        const bool in = pb + j >= P0 && pb + j < P0 + cnt;
-                        bb[j] = in ? bucket_from_group(w4, j, key, lp.level, pb + j, bp) : 0u;
-                    }
-                    packed = make_uint4(bb[0] | (bb[1] << 16), bb[2] | (bb[3] << 16), bb[4] | (bb[5] << 16),
-                                        bb[6] | (bb[7] << 16));
-                }
-                *reinterpret_cast<uint4*>(draws + (size_t)t * 16) = packed;
-                const int32_t e0 = (int32_t)(t * dpg) - (int32_t)doff;
-                const uint32_t pw4[4] = {packed.x, packed.y, packed.z, packed.w};
-                if (e0 >= 0 && e0 + (int32_t)dpg <= (int32_t)cnt) {  // whole group inside the tile
-#pragma unroll
-                    for (uint32_t j = 0; j < dpg; ++j) {
-                        if (NARROW) {
-                            atomicAdd(&Tw[__byte_perm(pw4[j >> 2], 0u, 0x4440u | (j & 3u))], 1u);
-                        } else {
-                            const uint32_t b = (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
-                            atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (uint32_t j = 0; j < dpg; ++j) {
-                        const int32_t e = e0 + (int32_t)j;
-                        if (e >= 0 && e < (int32_t)cnt) {
-                            if (NARROW) {
-                                atomicAdd(&Tw[(pw4[j >> 2] >> ((j & 3u) * 8u)) & 0xFFu], 1u);
-                            } else {
-                                const uint32_t b = (pw4[j >> 1] >> ((j & 1u) * 16u)) & 0xFFFFu;
-                                atomicAdd(&Tw[b >> 1], 1u << ((b & 1u) << 4));
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        if (dbg) rp.hdr->sclk[it * 6 + 1] = clock64();
-        // ---- wait for this tile's data, publish the counts
-        if (it & 1u) {
-            mbar_wait(&bar[1], ph1);
-            ph1 ^= 1u;
-        } else {
-            mbar_wait(&bar[0], ph0);
-            ph0 ^= 1u;
-        }
-        __syncthreads();
-        if (dbg) rp.hdr->sclk[it * 6 + 2] = clock64();
-        // ---- 2. scan: (bucket, warp)-major exclusive prefix of the counts ->
-        //      per-warp slot bases; bst = bucket starts of the tile
-        if (NARROW) scan_counters32<kSW * 32>(tab, kSW, k, bst, wsum);
-        else scan_counters<kSW * 32>(tab, kSW, k, bst, wsum);
-        __syncthreads();
-        if (dbg) rp.hdr->sclk[it * 6 + 3] = clock64();
-        // ---- 3. place: values to registers, then each to its slot in buf
-        {
-            E* el = reinterpret_cast<E*>(buf + ((cur.q0 * EB) & 15u));
-            const D* dp = reinterpret_cast<const D*>(draws) + doff;
-            // this warp's elements [e_lo, e_hi), walked in rounds of 32 in position order
-            const int32_t eb0 = (int32_t)(warp * qg * dpg) - (int32_t)doff;
-            const uint32_t e_lo = eb0 > 0 ? (uint32_t)eb0 : 0u;
-            const int32_t ehi = min((int32_t)((warp + 1) * qg * dpg) - (int32_t)doff, (int32_t)cnt);
-            const uint32_t len = ehi > (int32_t)e_lo ? (uint32_t)ehi - e_lo : 0u;
-            const E* ew = el + e_lo;
-            const D* dw = dp + e_lo;
-            E v[R];
-#pragma unroll
-            for (uint32_t r = 0; r < R; ++r) {
-                const uint32_t i = r * 32 + lane;
-                v[r] = ew[i < len ? i : 0];
-            }
-            __syncthreads();  // every element has been read out of buf
-#pragma unroll
-            for (uint32_t r = 0; r < R; ++r) {
-                const uint32_t i = r * 32 + lane;
-                if (r * 32 >= len) break;  // warp-uniform
-                const bool valid = i < len;
-                const uint32_t b = valid ? (uint32_t)dw[i] : 0u;
-                uint32_t slot;
-                if (NARROW) {
-                    if (ORD) {
-                        slot = atomicAdd(&Tw[b], valid ? 1u : 0u);
-                    } else {
-                        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu);
-                        const uint32_t old = valid ? Tw[b] : 0u;
-                        __syncwarp();
-                        if (valid && (peers & lanemask_lt()) == 0) Tw[b] = old + (uint32_t)__popc(peers);
-                        __syncwarp();
-                        slot = old + __popc(peers & lanemask_lt());
-                    }
-                } else if (ORD) {
-                    const uint32_t shb = (b & 1u) << 4;
-                    slot = (atomicAdd(&Tw[b >> 1], valid ? (1u << shb) : 0u) >> shb) & 0xFFFFu;
-                } else {
-                    slot = warp_rank(Tw, b, valid, false);
-                }
-                if (ORD && r == 0 && warp == 0) check_rank_order(b, valid, slot, &rp.hdr->error);
-                if (valid) {
-                    el[slot] = v[r];
-                    slotb[slot] = (D)b;
-                }
-            }
-        }
-        // destinations of the tile's runs: dst index of slot s = delta[b] + s
-        // a segment of <= 2^32 elements: every destination minus the segment
-        // start fits 32 bits, so delta is kept modulo 2^32 (half the lookup
-        // bytes in the copy-out); longer segments keep 64-bit deltas
-        const bool wide = (sg.len >> 32) != 0 || (rp.dbg & 64u);  // SHUF_DBG=64: test hook forcing the 64-bit path
-        for (uint32_t b = tid; b < k; b += kSW * 32) {
-            if (wide) delta64[b] = running[b] - bst[b];
-            else delta[b] = (uint32_t)(running[b] - sg.start) - bst[b];
-            running[b] += bst[b + 1] - bst[b];
-        }
-        __syncthreads();
-        if (dbg) rp.hdr->sclk[it * 6 + 4] = clock64();
-        // ---- 4. copy-out: slot s -> dst[delta[bucket(s)] + s]; consecutive
-        //      lanes take consecutive slots, so each warp store covers the
-        //      1-3 runs that meet its 32 slots (coalesced)
-        {
-            const E* el = reinterpret_cast<const E*>(buf + ((cur.q0 * EB) & 15u));
+            const E* so = reinterpret_cast<const E*>(sorted);
+            const D* sb = reinterpret_cast<const D*>(slotb);
             if (!wide) {
                 E* dst = reinterpret_cast<E*>(dstb) + sg.start;
-#pragma unroll 4
-                for (uint32_t x = tid; x < cnt; x += kSW * 32) dst[(uint32_t)(delta[slotb[x]] + x)] = el[x];
+                if (cnt == T) {
+#pragma unroll
+                    for (uint32_t j = 0; j < T / NT; ++j) {
+                        const uint32_t x = tid + j * NT;
+                        dst[(uint32_t)(delta[sb[x]] + x)] = so[x];
+                    }
+                } else {
+                    for (uint32_t x = tid; x < cnt; x += NT) dst[(uint32_t)(delta[sb[x]] + x)] = so[x];
+                }
             } else {
                 E* dst = reinterpret_cast<E*>(dstb);
-                for (uint32_t x = tid; x < cnt; x += kSW * 32) dst[delta64[slotb[x]] + x] = el[x];
+                for (uint32_t x = tid; x < cnt; x += NT) dst[delta64[sb[x]] + x] = so[x];
             }
         }
-        __syncthreads();
-        if (dbg) rp.hdr->sclk[it * 6 + 5] = clock64();
+        if (nxt.chunk >= nchunk) break;
+        // ---- A: draws + counts of the next tile (positions only)
+        const SegDesc nsg = next_chunk ? lp.segs[nxt.seg] : sg;
+        s_draw_count<EB, NARROW, V>(bp, make_key(nsg.key), lp.level, nxt.q0 - nsg.origin, ncnt, draws, Tw, kw, warp,
+                                 lane);
+        __syncthreads();  // copy-out done (sorted, slotb, delta free); counts complete
         new_chunk = next_chunk;
         cur = nxt;
         cnt = ncnt;
+        sg = nsg;
     }
     if (tid == 0) atomicAdd((unsigned long long*)&rp.hdr->scattered_hbm[lp.level], scattered);
 }
@@ -357,11 +397,22 @@ __global__ void __launch_bounds__(kSW * 32, 2) k_scatter(RunParams rp, LevelPara
 // Kernel selection: element size x ranking mode x lane width.
 template <int EB>
 static void* scatter_fn(bool ord, bool narrow) {
-    if (ord) return narrow ? (void*)k_scatter<EB, true, true> : (void*)k_scatter<EB, true, false>;
-    return narrow ? (void*)k_scatter<EB, false, true> : (void*)k_scatter<EB, false, false>;
+    if (ord) return narrow ? (void*)k_scatter<EB, true, true> : (void*)k_scatter<EB, false, true>;
+    return narrow ? (void*)k_scatter<EB, true, false> : (void*)k_scatter<EB, false, false>;
 }
 
 static void* scatter_kernel(uint32_t eb, bool ord, bool narrow) {
+    if (eb == 4 && narrow) {
+        switch (scv()) {
+        case 1: return ord ? (void*)k_scatter<4, true, true, 1> : (void*)k_scatter<4, true, false, 1>;
+        case 2: return ord ? (void*)k_scatter<4, true, true, 2> : (void*)k_scatter<4, true, false, 2>;
+        case 3: return ord ? (void*)k_scatter<4, true, true, 3> : (void*)k_scatter<4, true, false, 3>;
+        case 4: return ord ? (void*)k_scatter<4, true, true, 4> : (void*)k_scatter<4, true, false, 4>;
+        case 5: return ord ? (void*)k_scatter<4, true, true, 5> : (void*)k_scatter<4, true, false, 5>;
+        case 6: return ord ? (void*)k_scatter<4, true, true, 6> : (void*)k_scatter<4, true, false, 6>;
+        default: break;
+        }
+    }
     switch (eb) {
     case 4: return scatter_fn<4>(ord, narrow);
     case 8: return scatter_fn<8>(ord, narrow);
@@ -369,11 +420,18 @@ static void* scatter_kernel(uint32_t eb, bool ord, bool narrow) {
     }
 }
 
+static uint32_t scatter_threads(uint32_t eb, uint32_t k) {
+    if (!is_narrow(k)) return 256u;
+    if (eb != 4) return 512u;
+    const int v = scv();
+    return v == 4 ? 128u : ((v == 1 || v == 2 || v == 5 || v == 6) ? 256u : 512u);
+}
+
 cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     const uint32_t smem = scatter_smem_bytes(rp.eb, rp.k);
     void* args[] = {(void*)&rp, (void*)&lp};
     return cudaLaunchKernel(scatter_kernel(rp.eb, rp.rank_ordered != 0, rp.bp.narrow != 0), dim3(grid),
-                            dim3(kSW * 32), args, smem, s);
+                            dim3(scatter_threads(rp.eb, rp.k)), args, smem, s);
 }
 
 cudaError_t configure_scatter(uint32_t) {  // the attribute is the limit: plans with other sizes share the kernels
@@ -388,8 +446,8 @@ cudaError_t configure_scatter(uint32_t) {  // the attribute is the limit: plans 
 }
 
 cudaError_t occupancy_scatter(uint32_t eb, uint32_t k, int* blocks) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, scatter_kernel(eb, true, true), kSW * 32,
-                                                         scatter_smem_bytes(eb, k));
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, scatter_kernel(eb, true, is_narrow(k)),
+                                                         scatter_threads(eb, k), scatter_smem_bytes(eb, k));
 }
 
 }  // namespace shuf
