@@ -29,7 +29,6 @@
 // tile takes the checked path.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
 #include <type_traits>
 
 #include "block_ops.cuh"
@@ -37,30 +36,30 @@
 
 namespace shuf {
 
-// Tile geometry.  V selects an experimental variant (SHUF_SCV, u32 narrow only):
-// 0 = 32 KiB tiles x 16 warps (default), 1 = 32 KiB x 8 warps, 2 = 16 KiB x 8
-// warps, 3 = 16 KiB x 16 warps, 4 = 32 KiB x 4 warps, 5 = as 1 with packed u16
-// counters, 6 = 24 KiB x 8 warps.
-template <int EB, bool NARROW, int V = 0>
+// Tile geometry: 32 KiB tiles, 8 warps (R = T/256 rounds each), 2 CTAs per
+// SM.  Measured on HOT: 16 warps per tile, 16 KiB tiles (8 or
+// 16 warps), 24 KiB tiles x 3 CTAs/SM, 4 warps x 3 CTAs/SM and packed u16
+// counters were all slower -- the per-warp tables (zeroed and scanned every
+// tile, NW * k entries) cost more than the extra warps hide.
+template <int EB, bool NARROW>
 struct SCfg {
-    static constexpr uint32_t TB = (V == 2 || V == 3) ? 16384u : (V == 6 ? 24576u : kScatterTileBytes);
-    static constexpr uint32_t T = TB / EB;  // elements per tile
-    static constexpr uint32_t NW = V == 4 ? 4u : ((!NARROW || V == 1 || V == 2 || V == 5 || V == 6) ? 8u : 16u);
+    static constexpr uint32_t T = kScatterTileBytes / EB;  // elements per tile
+    static constexpr uint32_t NW = 8;
     static constexpr uint32_t NT = NW * 32u;
-    static constexpr uint32_t R = T / (NW * 32u);  // rounds per warp
+    static constexpr uint32_t R = T / (NW * 32u);     // rounds per warp
     static constexpr uint32_t sh = NARROW ? 4u : 3u;  // log2 draws per Philox group
     static constexpr uint32_t dpg = 1u << sh;
-    static constexpr bool P16 = !NARROW || V == 5;    // counters as packed u16 pairs (else u32)
-    static constexpr int MINB = !NARROW ? 1 : (V == 2 ? 4 : (V == 4 || V == 6 ? 3 : 2));
+    static constexpr bool P16 = !NARROW;              // counters as packed u16 pairs (k > 256), else u32
+    static constexpr int MINB = NARROW ? 2 : 1;
 };
 
 struct SLayout {
     uint32_t raw, sorted, draws, slotb, tab, bst, run, delta, wsum, bar, total;
 };
 
-template <int EB, bool NARROW, int V = 0>
+template <int EB, bool NARROW>
 __host__ __device__ inline SLayout s_layout(uint32_t k) {
-    using C = SCfg<EB, NARROW, V>;
+    using C = SCfg<EB, NARROW>;
     SLayout L;
     uint32_t off = 0;
     auto take = [&off](uint32_t bytes) {
@@ -85,29 +84,8 @@ __host__ __device__ inline SLayout s_layout(uint32_t k) {
 
 static bool is_narrow(uint32_t k) { return (k & (k - 1)) == 0 && k <= 256; }
 
-static int g_scv = -1;
-static int scv() {
-    if (g_scv < 0) {
-        const char* e = std::getenv("SHUF_SCV");
-        g_scv = e ? std::atoi(e) : 1;
-        if (g_scv < 0 || g_scv > 6) g_scv = 1;
-    }
-    return g_scv;
-}
-
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k) {
     const bool nr = is_narrow(k);
-    if (eb == 4 && nr) {
-        switch (scv()) {
-        case 1: return s_layout<4, true, 1>(k).total;
-        case 2: return s_layout<4, true, 2>(k).total;
-        case 3: return s_layout<4, true, 3>(k).total;
-        case 4: return s_layout<4, true, 4>(k).total;
-        case 5: return s_layout<4, true, 5>(k).total;
-        case 6: return s_layout<4, true, 6>(k).total;
-        default: break;
-        }
-    }
     switch (eb) {
     case 4: return nr ? s_layout<4, true>(k).total : s_layout<4, false>(k).total;
     case 8: return nr ? s_layout<8, true>(k).total : s_layout<8, false>(k).total;
@@ -168,11 +146,11 @@ __device__ __forceinline__ void s_issue_load(uint64_t q0, uint32_t cnt, const un
 // (16-byte group t holds the draws of positions ((P0 >> sh) + t) << sh ..),
 // and warp w's per-bucket counts of its element range (unordered shared
 // reductions on the warp's own table).
-template <int EB, bool NARROW, int V>
+template <int EB, bool NARROW>
 __device__ __forceinline__ void s_draw_count(const BucketParams& bp, PhiloxKey key, uint32_t level, uint64_t P0,
                                              uint32_t cnt, unsigned char* draws, uint32_t* Tw, uint32_t kw,
                                              uint32_t warp, uint32_t lane) {
-    using C = SCfg<EB, NARROW, V>;
+    using C = SCfg<EB, NARROW>;
     constexpr uint32_t sh = C::sh, dpg = C::dpg;
     for (uint32_t i = lane; i < kw; i += 32) Tw[i] = 0;
     __syncwarp();
@@ -230,13 +208,13 @@ __device__ __forceinline__ void s_draw_count(const BucketParams& bp, PhiloxKey k
 }
 
 // C: rank + place of warp w's rounds.  FULL: cnt == T (no checks).
-template <int EB, bool NARROW, bool ORD, bool FULL, int V>
+template <int EB, bool NARROW, bool ORD, bool FULL>
 __device__ __forceinline__ void s_place(const unsigned char* raw, uint64_t q0, const unsigned char* draws,
                                         uint32_t doff, uint32_t cnt, unsigned char* sorted, unsigned char* slotb_,
                                         uint32_t* Tw, uint32_t warp, uint32_t lane, uint32_t* err) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
-    using C = SCfg<EB, NARROW, V>;
+    using C = SCfg<EB, NARROW>;
     const uint32_t e0 = warp * C::R * 32u;
     const E* el = reinterpret_cast<const E*>(raw + ((q0 * EB) & 15u)) + e0 + lane;
     const D* dp = reinterpret_cast<const D*>(draws) + doff + e0 + lane;
@@ -275,16 +253,16 @@ __device__ __forceinline__ void s_place(const unsigned char* raw, uint64_t q0, c
     }
 }
 
-template <int EB, bool NARROW, bool ORD, int V = 0>
-__global__ void __launch_bounds__(SCfg<EB, NARROW, V>::NT, SCfg<EB, NARROW, V>::MINB)
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(SCfg<EB, NARROW>::NT, SCfg<EB, NARROW>::MINB)
     k_scatter(RunParams rp, LevelParams lp) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
-    using C = SCfg<EB, NARROW, V>;
+    using C = SCfg<EB, NARROW>;
     constexpr uint32_t T = C::T, NT = C::NT;
     extern __shared__ __align__(16) unsigned char sm[];
     const uint32_t k = rp.k, kw = C::P16 ? (k + 1) >> 1 : k;  // table words per warp
-    const SLayout Ly = s_layout<EB, NARROW, V>(k);
+    const SLayout Ly = s_layout<EB, NARROW>(k);
     unsigned char* raw = sm + Ly.raw;
     unsigned char* sorted = sm + Ly.sorted;
     unsigned char* draws = sm + Ly.draws;
@@ -317,7 +295,7 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW, V>::NT, SCfg<EB, NARROW, V>::
     unsigned long long scattered = cur.q1 - cur.q0;
     s_issue_load<EB>(cur.q0, cnt, src, raw, &bar[0]);
     SegDesc sg = lp.segs[cur.seg];
-    s_draw_count<EB, NARROW, V>(bp, make_key(sg.key), lp.level, cur.q0 - sg.origin, cnt, draws, Tw, kw, warp, lane);
+    s_draw_count<EB, NARROW>(bp, make_key(sg.key), lp.level, cur.q0 - sg.origin, cnt, draws, Tw, kw, warp, lane);
     bool new_chunk = true;
     __syncthreads();
     for (;;) {
@@ -344,10 +322,10 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW, V>::NT, SCfg<EB, NARROW, V>::
         ph ^= 1u;
         const uint32_t doff = (uint32_t)((cur.q0 - sg.origin) & (C::dpg - 1));
         if (cnt == T)
-            s_place<EB, NARROW, ORD, true, V>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
+            s_place<EB, NARROW, ORD, true>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
                                            &rp.hdr->error);
         else
-            s_place<EB, NARROW, ORD, false, V>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
+            s_place<EB, NARROW, ORD, false>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
                                             &rp.hdr->error);
         __syncthreads();  // raw consumed; sorted, slotb and delta complete
         // ---- next tile of this CTA's sequence: load it into the raw buffer
@@ -383,7 +361,7 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW, V>::NT, SCfg<EB, NARROW, V>::
         if (nxt.chunk >= nchunk) break;
         // ---- A: draws + counts of the next tile (positions only)
         const SegDesc nsg = next_chunk ? lp.segs[nxt.seg] : sg;
-        s_draw_count<EB, NARROW, V>(bp, make_key(nsg.key), lp.level, nxt.q0 - nsg.origin, ncnt, draws, Tw, kw, warp,
+        s_draw_count<EB, NARROW>(bp, make_key(nsg.key), lp.level, nxt.q0 - nsg.origin, ncnt, draws, Tw, kw, warp,
                                  lane);
         __syncthreads();  // copy-out done (sorted, slotb, delta free); counts complete
         new_chunk = next_chunk;
@@ -402,17 +380,6 @@ static void* scatter_fn(bool ord, bool narrow) {
 }
 
 static void* scatter_kernel(uint32_t eb, bool ord, bool narrow) {
-    if (eb == 4 && narrow) {
-        switch (scv()) {
-        case 1: return ord ? (void*)k_scatter<4, true, true, 1> : (void*)k_scatter<4, true, false, 1>;
-        case 2: return ord ? (void*)k_scatter<4, true, true, 2> : (void*)k_scatter<4, true, false, 2>;
-        case 3: return ord ? (void*)k_scatter<4, true, true, 3> : (void*)k_scatter<4, true, false, 3>;
-        case 4: return ord ? (void*)k_scatter<4, true, true, 4> : (void*)k_scatter<4, true, false, 4>;
-        case 5: return ord ? (void*)k_scatter<4, true, true, 5> : (void*)k_scatter<4, true, false, 5>;
-        case 6: return ord ? (void*)k_scatter<4, true, true, 6> : (void*)k_scatter<4, true, false, 6>;
-        default: break;
-        }
-    }
     switch (eb) {
     case 4: return scatter_fn<4>(ord, narrow);
     case 8: return scatter_fn<8>(ord, narrow);
@@ -420,12 +387,7 @@ static void* scatter_kernel(uint32_t eb, bool ord, bool narrow) {
     }
 }
 
-static uint32_t scatter_threads(uint32_t eb, uint32_t k) {
-    if (!is_narrow(k)) return 256u;
-    if (eb != 4) return 512u;
-    const int v = scv();
-    return v == 4 ? 128u : ((v == 1 || v == 2 || v == 5 || v == 6) ? 256u : 512u);
-}
+static uint32_t scatter_threads(uint32_t, uint32_t) { return SCfg<4, true>::NT; }
 
 cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     const uint32_t smem = scatter_smem_bytes(rp.eb, rp.k);
