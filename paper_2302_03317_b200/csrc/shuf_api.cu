@@ -272,10 +272,20 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     if (target < 1) target = 1;
     if (target > 4096) target = 4096;
     uint64_t C = (n + target - 1) / target;
+    {  // SHUF_CHUNK=<elements>: another chunk size (test hook: the result must not depend on it)
+        const char* ce = std::getenv("SHUF_CHUNK");
+        const long long v = ce ? std::atoll(ce) : 0;
+        if (v > 0) C = (uint64_t)v;
+    }
     C = align_up(C < T ? T : C, T);
     if (C > 0x40000000ull) C = 0x40000000ull;
     p->chunk = (uint32_t)C;
     p->levels = plan_levels(n, k, S);
+    {  // SHUF_LEVELS=<n>: fewer planned HBM levels (test hook for the device depth check)
+        const char* le = std::getenv("SHUF_LEVELS");
+        const long v = le ? std::atol(le) : -1;
+        if (v >= 0 && (uint32_t)v < p->levels) p->levels = (uint32_t)v;
+    }
     {
         const char* df = std::getenv("SHUF_DEFER");
         p->defer_planned = (df && df[0] == '1') ? 1 : 0;
@@ -381,6 +391,16 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     p->grid_small = p->sms * 4;
     p->grid_fast = p->sms;
     p->grid_leaf = p->sms * clamp1(ol);
+    {  // SHUF_GRID=<ctas>: cap every persistent grid (test hook: the result must not depend on it)
+        const char* ge = std::getenv("SHUF_GRID");
+        const int g = ge ? std::atoi(ge) : 0;
+        if (g > 0) {
+            int* grids[] = {&p->grid_hist, &p->grid_scan, &p->grid_scatter, &p->grid_finish, &p->grid_small,
+                            &p->grid_fast, &p->grid_leaf};
+            for (int* q : grids)
+                if (*q > g) *q = g;
+        }
+    }
     p->dev_ready = true;
     return cudaSuccess;
 }

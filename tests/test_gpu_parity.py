@@ -233,3 +233,61 @@ def test_alternate_routes_bit_exact(env):
     r = subprocess.run([sys.executable, "-c", _ENV_CASES % root], env=dict(os.environ, **env), capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+_INVARIANCE_CASES = (
+    "import sys; sys.path.insert(0, %r)\n"
+    "import numpy as np, oracle, synth\n"
+    "from tests.gpu_util import gpu_shuffle, gpu_segmented\n"
+    "for n, k, L, seed in [(3_000_000, 256, 4096, 11), (1 << 23, 64, 300, 21), (777_777, 7, 300, 6),\n"
+    "                      (300_001, 1000, 50, 7), (200_000, 2, 1, 8)]:\n"
+    "    a = np.arange(n, dtype=np.uint32)\n"
+    "    assert (gpu_shuffle(a, k, L, seed) == oracle.shuffle(a, k, L, seed)).all(), (n, k, L, seed)\n"
+    "b = synth.splitmix64_stream_np(3, 0, 1_000_003)\n"
+    "assert (gpu_shuffle(b, 256, 1000, 12) == oracle.shuffle(b, 256, 1000, 12)).all()\n"
+    "off = np.array([0, 0, 1, 3000, 300000, 309001, 900000], dtype=np.uint64)\n"
+    "d = np.arange(int(off[-1]), dtype=np.uint32)\n"
+    "assert (gpu_segmented(d, off, 64, 4096, 5) == oracle.segmented(d, off, 64, 4096, 5)).all()\n"
+    "print('ok')\n")
+
+
+@pytest.mark.parametrize("env", [{"SHUF_SFUSE": "5000"}, {"SHUF_CHUNK": "8192"}, {"SHUF_CHUNK": "1000000"},
+                                 {"SHUF_GRID": "7"}, {"SHUF_GRID": "1", "SHUF_CHUNK": "40000"}],
+                         ids=["sfuse5000", "chunk8192", "chunk1M", "grid7", "grid1"])
+def test_schedule_invariance_bit_exact(env):
+    """The permutation is a function of (n, k, L, seed) only (D6; the paper's
+    schedule independence): the fused size, the chunk size and the
+    persistent grid size change which kernel does what and in which order, not
+    the bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _INVARIANCE_CASES % root], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_depth_overflow_is_reported():
+    """A child still longer than the fused size after the last planned HBM
+    level must surface as SHUF_ERR_DEPTH through shuf_last_device_error
+    (include/shuf.h: callers must check it) -- forced here by planning one HBM
+    level (SHUF_LEVELS=1) for a problem that needs two."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import numpy as np\n"
+            "from tests.gpu_util import gpu_shuffle\n"
+            "import paper_2302_03317_b200 as shuf, torch\n"
+            "a = np.arange(1 << 23, dtype=np.uint32)\n"
+            "x = torch.from_numpy(a.view(np.int32)).cuda()\n"
+            "p = shuf.shuf_plan(a.shape[0], 4, 64, 300, 21)\n"
+            "assert p.planned_levels == 1\n"
+            "s = torch.empty(p.scratch_bytes, dtype=torch.uint8, device='cuda')\n"
+            "shuf.shuf_run(p, x, s)\n"
+            "print('err', shuf.shuf_last_device_error(p))\n" % root)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SHUF_LEVELS="1"), capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "err 5" in r.stdout, r.stdout + r.stderr
