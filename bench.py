@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="hot", choices=["hot", "c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--mode", default="stable", choices=["stable", "inplace"],
+                    help="inplace: shuf_run_inplace (SURVEY 8(a) a10; aux memory instead of the ping-pong buffer)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 25)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
@@ -217,12 +219,20 @@ def main():
         d_off = None
         x = synth.make_input_torch(w, dev)
     plan = shuf.shuf_plan(w.n, w.elem_bytes, w.k, w.L, seed)
-    scratch = torch.empty(plan.scratch_bytes if d_off is None else plan.scratch_bytes_segmented(d_off.numel() - 1),
-                          dtype=torch.uint8, device=dev)
+    inplace = args.mode == "inplace"
+    if inplace and d_off is not None:
+        raise SystemExit("--mode inplace: single-shuffle workloads only")
+    if inplace:
+        scratch = torch.empty(max(1, shuf.shuf_aux_bytes_inplace(plan)), dtype=torch.uint8, device=dev)
+    else:
+        scratch = torch.empty(plan.scratch_bytes if d_off is None else plan.scratch_bytes_segmented(d_off.numel() - 1),
+                              dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        if d_off is None:
+        if inplace:
+            shuf.shuf_run_inplace(plan, x, scratch, stream)
+        elif d_off is None:
             shuf.shuf_run(plan, x, scratch, stream)
         else:
             shuf.shuf_segmented(plan, x, d_off, scratch, stream)
@@ -257,7 +267,11 @@ def main():
     eff_gbps = eff_bytes / (ms / 1e3) / 1e9
 
     # ---- per-kernel breakdown (separate pass; every launch bracketed by events on `stream`)
-    prof = shuf.shuf_profile_run(plan, x, scratch, d_off, stream)
+    if inplace:  # the in-place mode synchronises per level: no per-kernel split, the step is the unit
+        prof = {c: (0.0, 0) for c in shuf.KERNEL_CLASSES}
+        prof["scatter"] = (ms, 1)
+    else:
+        prof = shuf.shuf_profile_run(plan, x, scratch, d_off, stream)
     peaks, peak_src = load_peaks()
     hbm_peak = float(peaks["hbm_gbs"])
     eb = w.elem_bytes
@@ -270,9 +284,11 @@ def main():
             d["algorithmic_bytes"] = kbytes[name]
             d["GBps"] = round(kbytes[name] / (kms / 1e3) / 1e9, 1)
         kernels[name] = d
+    if inplace:  # whole step against the measured copy bandwidth
+        kbytes["scatter"] = eff_bytes
     dom = max(("scatter", "finish", "leaf"), key=lambda c: prof[c][0])
     dms, dcnt = prof[dom]
-    if dom == "scatter":  # planned-but-empty trailing levels launch and exit at once: count the real ones
+    if dom == "scatter" and not inplace:  # planned-but-empty trailing levels launch and exit at once: count the real ones
         dcnt = max(1, sum(1 for v in stats["scattered_hbm"] if v > 0))
     achieved = kbytes[dom] / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     traffic = None
@@ -287,10 +303,12 @@ def main():
                 "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                 "algorithmic_bytes_per_launch": kbytes[dom] / max(1, dcnt),
                 "avg_launch_ms": dms / max(1, dcnt)}
+    if inplace:
+        roofline["kernel"] = "whole in-place step (Q11 bytes)"
 
     # ---- end to end through the C ABI with host buffers (pinned), copies timed
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not inplace:
         # every step copies its input in from pinned host memory and its result
         # back out; two device buffers let step i+1's upload and step i-1's
         # download run (full duplex) while step i shuffles
@@ -351,7 +369,8 @@ def main():
                        "elem_bytes": w.elem_bytes, "k": w.k, "L": w.L, "seed": w.seed,
                        "l2": "inputs larger than L2 (no flush)" if w.n * w.elem_bytes > (256 << 20)
                        else "input fits in L2: not an HBM figure",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "mode": args.mode},
             "eff_GBps": eff_gbps, "frac_of_8TBps": eff_gbps / SPEC_HBM_GBPS,
             "frac_of_measured_copy": eff_gbps / hbm_peak, "effective_bytes_per_step": eff_bytes,
             "elements_scattered_per_step": scattered, "levels": {"hbm": stats["scattered_hbm"],

@@ -185,6 +185,22 @@ shuf_status shuf_debug_clocks(shuf_plan_t p, void *stream, long long *out, uint3
  * if none), clearing it. */
 shuf_status shuf_last_device_error(shuf_plan_t p, void *stream);
 
+/* Hidden-constant simulation (section 7,
+ * P:773-788, of Lemma 2 P:284-296 and Lemma 4 / Corollary 5 P:392-416),
+ * DESIGN.md D9.  For run r = 0 .. runs-1 with key K(seed, r): RoughScatter
+ * on n items into k buckets of capacities c_i = floor((i+1)n/k)
+ * - floor(i n/k), iteration t placing one item into bucket D4 draw (level 0,
+ * position t), stopping when a bucket is full; d_T[r] = items placed T (the
+ * Lemma-2 remainder is R = n - T).  The remaining draws t = T .. n-1 complete
+ * the final sizes n^f; d_M[r] = sum_i |D_i| with D_i the prefix sums of
+ * n^f_i - c_i (TwoSweep's swaps, Lemma 4).  d_T, d_M: DEVICE arrays of runs
+ * uint64, 8-byte aligned, owned by the caller.  2 <= k <= 2^16 and n >= k
+ * (SHUF_ERR_INVALID_ARG); k > 2^15 needs n/k well below 2^16
+ * (SHUF_ERR_UNSUPPORTED).  Stream-ordered; exact integers (bit-identical to
+ * the oracle's oracle_sim_rough_scatter). */
+shuf_status shuf_sim_rough_scatter(uint64_t n, uint32_t k, uint64_t seed, uint32_t runs, uint64_t *d_T,
+                                   uint64_t *d_M, void *stream);
+
 /* The cudaError_t behind the last SHUF_ERR_CUDA returned for this plan. */
 int shuf_last_cuda_error(shuf_plan_t p);
 

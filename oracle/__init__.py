@@ -86,6 +86,8 @@ def lib():
         L.oracle_segmented.restype = i32
         L.oracle_points.argtypes = [u64, u32, u32, u64, vp, u64, vp]
         L.oracle_points.restype = i32
+        L.oracle_sim_rough_scatter.argtypes = [u64, u32, u64, u32, vp, vp]
+        L.oracle_sim_rough_scatter.restype = i32
         _lib = L
     return _lib
 
@@ -201,3 +203,15 @@ def points(n: int, k: int, L: int, seed: int, js) -> np.ndarray:
     if rc:
         raise RuntimeError(f"oracle_points failed with status {rc}")
     return out
+
+
+def sim_rough_scatter(n: int, k: int, seed: int, runs: int):
+    """D9 (NEXT-1): per run r (key K(seed, r)) the RoughScatter stop
+    time T (items placed when the first bucket fills, Lemma 2: R = n - T) and
+    the TwoSweep swap count M = sum_i |D_i| (Lemma 4).  Returns (T, M)."""
+    T = np.zeros(runs, dtype=np.uint64)
+    M = np.zeros(runs, dtype=np.uint64)
+    rc = lib().oracle_sim_rough_scatter(n, k, seed, runs, _ptr(T), _ptr(M))
+    if rc:
+        raise RuntimeError(f"oracle_sim_rough_scatter failed with status {rc}")
+    return T, M

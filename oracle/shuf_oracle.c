@@ -609,3 +609,59 @@ int oracle_points(uint64_t n, uint32_t k, uint32_t L, uint64_t seed, const uint6
     free(qs); free(qp);
     return rc;
 }
+
+/* ------------------------------------------------- D9 (NEXT-1) -- */
+/* Hidden-constant simulation of Lemma 2 and Corollary 5 / Lemma
+ * 4, one run per key K(seed, r) (D2), r = 0 .. runs-1:
+ *
+ *   RoughScatter on n items and k buckets of capacities
+ *   c_i = floor((i+1) n / k) - floor(i n / k) ("equal sizes n/k up to
+ *   rounding"): in iteration t = 0, 1, ... draw the partner bucket
+ *   j_t uniformly from [0, k) -- here the D4 bucket draw at level 0 and
+ *   position t (the path's own generator) -- and place one item into B_j
+ *   (s_j += 1); stop as soon as B_j is full (s_j = c_j).  T = number of
+ *   placed items, R = n - T the items left staged (Lemma 2).
+ *
+ *   Final bucket sizes ("run the balls-into-bins experiment to
+ *   completion"): the remaining R items draw j_t for t = T .. n-1
+ *   the same way, n^f_i = #{t < n : j_t = i}.  d_i = n^f_i - c_i (deviation
+ *   from the initial estimate), D_i = d_0 + ... + d_i, and TwoSweep performs
+ *   M = sum_i |D_i| swaps (Lemma 4).
+ *
+ * Writes T[r] and M[r].  Returns 0, or ERR_INVALID_ARG for k < 2, k > 2^16
+ * or n < k (every bucket needs capacity >= 1).                               */
+int oracle_sim_rough_scatter(uint64_t n, uint32_t k, uint64_t seed, uint32_t runs, uint64_t *T, uint64_t *M)
+{
+    if (k < 2 || k > 65536u || n < k) return ORACLE_ERR_INVALID_ARG;
+    uint64_t *s = (uint64_t *)malloc((size_t)k * sizeof(uint64_t));
+    if (!s) return ORACLE_ERR_NOMEM;
+    for (uint32_t r = 0; r < runs; ++r) {
+        const uint64_t K = oracle_problem_key(seed, r);
+        memset(s, 0, (size_t)k * sizeof(uint64_t));
+        uint64_t t = 0, stop = n;
+        for (; t < n; ++t) {                        /* RoughScatter iterations */
+            const uint32_t j = oracle_bucket_draw(K, 0, t, k, NULL);
+            const uint64_t cj = (uint64_t)(((unsigned __int128)(j + 1) * n) / k) -
+                                (uint64_t)(((unsigned __int128)j * n) / k);
+            s[j] += 1;
+            if (s[j] == cj) {                       /* B_j is full: stop */
+                stop = t + 1;
+                ++t;
+                break;
+            }
+        }
+        for (; t < n; ++t) s[oracle_bucket_draw(K, 0, t, k, NULL)] += 1; /* the staged rest */
+        int64_t D = 0;
+        uint64_t m = 0;
+        for (uint32_t i = 0; i < k; ++i) {
+            const uint64_t ci = (uint64_t)(((unsigned __int128)(i + 1) * n) / k) -
+                                (uint64_t)(((unsigned __int128)i * n) / k);
+            D += (int64_t)s[i] - (int64_t)ci;
+            m += (uint64_t)(D < 0 ? -D : D);
+        }
+        T[r] = stop;
+        M[r] = m;
+    }
+    free(s);
+    return 0;
+}

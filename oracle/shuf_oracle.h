@@ -35,5 +35,6 @@ int oracle_segmented(void *data, const uint64_t *offsets, uint64_t num_segments,
 
 int oracle_points(uint64_t n, uint32_t k, uint32_t L, uint64_t seed, const uint64_t *js, uint64_t count,
                   uint64_t *out);
+int oracle_sim_rough_scatter(uint64_t n, uint32_t k, uint64_t seed, uint32_t runs, uint64_t *T, uint64_t *M);
 
 #endif

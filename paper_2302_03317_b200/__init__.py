@@ -24,7 +24,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libshuf.so")
+lib_path = os.environ.get("SHUF_LIB_PATH") or os.path.join(_HERE, "libshuf.so")  # env: experiments only
 _lib = None
 
 STATUS = {0: "SHUF_OK", 1: "SHUF_ERR_INVALID_ARG", 2: "SHUF_ERR_UNSUPPORTED", 3: "SHUF_ERR_ALIGNMENT",
@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
     "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks", "shuf_aux_bytes_inplace", "shuf_run_inplace",
-    "shuf_debug_inplace_levels", "shuf_scratch_bytes_segmented",
+    "shuf_debug_inplace_levels", "shuf_scratch_bytes_segmented", "shuf_sim_rough_scatter",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish", "leaf"]
 
@@ -64,6 +64,8 @@ def lib():
         L.shuf_last_status.restype = i32
         L.shuf_scratch_bytes.argtypes = [vp, ctypes.POINTER(u64)]
         L.shuf_scratch_bytes.restype = i32
+        L.shuf_sim_rough_scatter.argtypes = [u64, u32, u64, u32, vp, vp, vp]
+        L.shuf_sim_rough_scatter.restype = i32
         L.shuf_scratch_bytes_segmented.argtypes = [vp, u64, ctypes.POINTER(u64)]
         L.shuf_scratch_bytes_segmented.restype = i32
         L.shuf_run.argtypes = [vp, vp, vp, u64, vp]
@@ -238,6 +240,13 @@ def shuf_debug_fy_draws(K: int, q, i, out, stream=None):
     """D5 partners of steps i of the leaves starting at q (device arrays)."""
     _check(lib().shuf_debug_fy_draws(K % (1 << 64), _dev_ptr(q, "q"), _dev_ptr(i, "i"), q.numel(),
                                      _dev_ptr(out, "out"), _stream(stream)), "shuf_debug_fy_draws")
+
+
+def shuf_sim_rough_scatter(n: int, k: int, seed: int, runs: int, d_T, d_M, stream=None):
+    """Hidden-constant simulation (NEXT-1): per run the RoughScatter
+    stop time T and the TwoSweep swap count M into int64 CUDA tensors of runs."""
+    _check(lib().shuf_sim_rough_scatter(n, k, seed % (1 << 64), runs, _dev_ptr(d_T, "T"), _dev_ptr(d_M, "M"),
+                                        _stream(stream)), "shuf_sim_rough_scatter")
 
 
 def shuf_last_device_error(plan: Plan, stream=None) -> int:

@@ -50,7 +50,10 @@ struct SCfg {
     static constexpr uint32_t sh = NARROW ? 4u : 3u;  // log2 draws per Philox group
     static constexpr uint32_t dpg = 1u << sh;
     static constexpr bool P16 = !NARROW;              // counters as packed u16 pairs (k > 256), else u32
-    static constexpr int MINB = NARROW ? 2 : 1;
+#ifndef SHUF_SCATTER_MINB
+#define SHUF_SCATTER_MINB 2
+#endif
+    static constexpr int MINB = NARROW ? SHUF_SCATTER_MINB : 1;
 };
 
 struct SLayout {

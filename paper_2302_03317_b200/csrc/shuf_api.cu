@@ -38,6 +38,9 @@ struct shuf_plan_s {
     int sms;
     int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small, grid_fast, grid_leaf;
     int fast, leafk, defer;
+    int hist_overlap;             // 1: level l+1's histogram runs on side_stream during level l's scatter
+    cudaStream_t side_stream;
+    cudaEvent_t ev_fork, ev_join;
     bool ip_ready;
     int grid_ipc, grid_ipp;
     int rank_ordered;
@@ -378,6 +381,18 @@ static cudaError_t device_setup(shuf_plan_s* p) {
         const char* df = std::getenv("SHUF_DEFER");
         p->defer = (p->leafk && p->defer_planned && df && df[0] == '1') ? 1 : 0;
     }
+    // the next level's histogram (reads no data: positions only) on a side
+    // stream, overlapping the current level's scatter (SHUF_HIST_OVERLAP=1; off by
+    // default: the scatter holds every register of the SM, so the two do not co-run)
+    {
+        const char* ho = std::getenv("SHUF_HIST_OVERLAP");
+        p->hist_overlap = (ho && ho[0] == '1') ? 1 : 0;  // measured: no gain
+        if (p->hist_overlap) {
+            if ((e = cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking))) return e;
+            if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) return e;
+            if ((e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming))) return e;
+        }
+    }
     // persistent grids: SM count x resident CTAs per SM
     int oh = 1, os = 1, osc = 1, of = 1, ol = 1;
     if ((e = occupancy_level(p->eb, p->k, &oh, &os, &osc))) return e;
@@ -534,11 +549,25 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         }
     }
     const uint32_t G = p->levels < max_levels ? p->levels : max_levels;
+    // level l+1's histogram needs only k_plan(l)'s list, so it is forked onto
+    // the side stream before level l's scatter and joined before scan(l+1)
+    // (fork/join inside the call: still stream-ordered for the caller)
+    const bool overlap = p->hist_overlap && !prof;
     for (uint32_t lv = 0; lv < G; ++lv) {
         const LevelParams lp = level_params(lay, sc, buf0, lv);
-        LAUNCH(SHUF_K_HIST, launch_hist(rp, lp, st, p->grid_hist));
+        if (overlap && lv > 0) {
+            if ((e = cudaStreamWaitEvent(st, p->ev_join, 0))) return cuda_fail(p, e);
+        } else {
+            LAUNCH(SHUF_K_HIST, launch_hist(rp, lp, st, p->grid_hist));
+        }
         LAUNCH(SHUF_K_SCAN, launch_scan(rp, lp, st, p->grid_scan));
         LAUNCH(SHUF_K_PLAN, launch_plan(rp, lp, st, p->grid_small));
+        if (overlap && lv + 1 < G) {
+            if ((e = cudaEventRecord(p->ev_fork, st))) return cuda_fail(p, e);
+            if ((e = cudaStreamWaitEvent(p->side_stream, p->ev_fork, 0))) return cuda_fail(p, e);
+            LAUNCH(SHUF_K_HIST, launch_hist(rp, level_params(lay, sc, buf0, lv + 1), p->side_stream, p->grid_hist));
+            if ((e = cudaEventRecord(p->ev_join, p->side_stream))) return cuda_fail(p, e);
+        }
         LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
         if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast(rp, lp, st, p->grid_fast));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
@@ -782,6 +811,22 @@ extern "C" shuf_status shuf_debug_bucket_draws(uint64_t K, uint32_t level, uint6
     return e ? SHUF_ERR_CUDA : SHUF_OK;
 }
 
+extern "C" shuf_status shuf_sim_rough_scatter(uint64_t n, uint32_t k, uint64_t seed, uint32_t runs, uint64_t* d_T,
+                                              uint64_t* d_M, void* stream) {
+    if (k < 2 || k > 65536 || n < k || (runs && (!d_T || !d_M))) return SHUF_ERR_INVALID_ARG;
+    if (((uintptr_t)d_T & 7u) || ((uintptr_t)d_M & 7u)) return SHUF_ERR_ALIGNMENT;
+    if (k > 32768) {  // packed u16 counters: every final bucket count must stay below 2^16
+        const double m = (double)n / k;
+        if (m + 8.0 * std::sqrt(m) + 64.0 >= 65536.0) return SHUF_ERR_UNSUPPORTED;
+    }
+    if (runs == 0) return SHUF_OK;
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (!e) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!e) e = launch_sim_rough(n, k, seed, runs, d_T, d_M, sms * 8, static_cast<cudaStream_t>(stream));
+    return e ? SHUF_ERR_CUDA : SHUF_OK;
+}
+
 extern "C" shuf_status shuf_debug_fy_draws(uint64_t K, const uint64_t* d_P, const uint32_t* d_s, uint64_t count,
                                            uint32_t* d_out, void* stream) {
     if (count && (!d_P || !d_s || !d_out)) return SHUF_ERR_INVALID_ARG;
@@ -823,7 +868,14 @@ extern "C" shuf_status shuf_last_run_stats(shuf_plan_t p, void* stream, uint64_t
     return SHUF_OK;
 }
 
-extern "C" void shuf_destroy(shuf_plan_t p) { delete p; }
+extern "C" void shuf_destroy(shuf_plan_t p) {
+    if (p && p->dev_ready && p->hist_overlap) {
+        cudaStreamDestroy(p->side_stream);
+        cudaEventDestroy(p->ev_fork);
+        cudaEventDestroy(p->ev_join);
+    }
+    delete p;
+}
 
 extern "C" const char* shuf_status_string(shuf_status s) {
     switch (s) {

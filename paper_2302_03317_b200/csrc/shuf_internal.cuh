@@ -220,6 +220,8 @@ cudaError_t occupancy_scatter(uint32_t eb, uint32_t k, int* blocks);
 cudaError_t configure_finish(uint32_t smem);
 cudaError_t occupancy_level(uint32_t eb, uint32_t k, int* hist, int* scan, int* scatter);
 cudaError_t occupancy_finish(uint32_t eb, uint32_t smem, int* blocks);
+cudaError_t launch_sim_rough(uint64_t n, uint32_t k, uint64_t seed, uint32_t runs, uint64_t* T, uint64_t* M, int grid,
+                             cudaStream_t s);
 cudaError_t launch_debug_bucket_draws(uint64_t K, uint32_t level, uint64_t p0, uint64_t count, uint32_t k,
                                       uint32_t* d_out, cudaStream_t s);
 cudaError_t launch_debug_fy_draws(uint64_t K, const uint64_t* d_P, const uint32_t* d_s, uint64_t count,
