@@ -94,16 +94,24 @@ struct Leaf {
     uint64_t start, len, origin, key;
 };
 
-// Leaf `lane` of unit u of a level's children: children 32g .. 32g+31 of
-// segment s, u = s * ceil(k/32) + g.
+// Units of U leaves per warp: U = 32 (lane x owns leaf x of the unit) when
+// leaves are short, U = 1 when leaves of about L/2 or more already take the
+// warp-cooperative path -- then one long leaf per warp-unit spreads the long
+// leaves over all warps instead of 32 of them over one warp.
+__host__ __device__ inline uint32_t leaf_unit(uint32_t eb, uint32_t L) {
+    return 8u * ((L / 2u) * eb + 32u) > leaf_slot_bytes(eb, L) ? 1u : 32u;
+}
+
+// Leaf `lane` of unit u of a level's children: children U*g .. U*g+U-1 of
+// segment s, u = s * ceil(k/U) + g.
 struct ChildLeaves {
     const LevelParams* lp;
-    uint32_t k, groups;
+    uint32_t k, groups, U;
     __device__ __forceinline__ uint64_t units() const { return (uint64_t)lp->ctr->nseg * groups; }
     __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
         Leaf f{0, 0, 0, 0};
-        const uint32_t s = (uint32_t)(u / groups), b = (uint32_t)(u % groups) * 32u + lane;
-        if (b < k) {
+        const uint32_t s = (uint32_t)(u / groups), b = (uint32_t)(u % groups) * U + lane;
+        if (lane < U && b < k) {
             const SegDesc sg = lp->segs[s];
             const uint64_t base0 = lp->prefix[sg.cbase];
             const uint64_t s0 = lp->prefix[sg.cbase + (uint64_t)b * sg.nchunks] - base0;
@@ -117,15 +125,16 @@ struct ChildLeaves {
     }
 };
 
-// User segments 32u .. 32u+31 (segmented mode at level 0, or the root).
+// User segments U*u .. U*u+U-1 (segmented mode at level 0, or the root).
 struct SegLeaves {
     const uint64_t* off;
     uint64_t nsegs, seed;
-    __device__ __forceinline__ uint64_t units() const { return (nsegs + 31) / 32; }
+    uint32_t U;
+    __device__ __forceinline__ uint64_t units() const { return (nsegs + U - 1) / U; }
     __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
         Leaf f{0, 0, 0, 0};
-        const uint64_t s = u * 32u + lane;
-        if (s < nsegs) {
+        const uint64_t s = u * U + lane;
+        if (lane < U && s < nsegs) {
             f.start = off[s];
             const uint64_t e = off[s + 1];
             f.len = e > f.start ? e - f.start : 0;
@@ -310,14 +319,15 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_children(RunParams rp, LevelParams lp) {
-    const ChildLeaves ls{&lp, rp.k, (rp.k + 31) / 32};
+    const uint32_t U = leaf_unit(EB, rp.L);
+    const ChildLeaves ls{&lp, rp.k, (rp.k + U - 1) / U, U};
     run_leaves<EB>(rp, lp.dst, ls, leaf_slot_bytes(EB, rp.L));
 }
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_segments(RunParams rp, const uint64_t* __restrict__ off,
                                                                  uint64_t nsegs) {
-    const SegLeaves ls{off, nsegs, rp.seed};
+    const SegLeaves ls{off, nsegs, rp.seed, leaf_unit(EB, rp.L)};
     run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
 }
 
