@@ -43,12 +43,27 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False, extra=()) -> str:
     if not force and not stale():
         return LIB
+    # One nvcc per translation unit, in parallel, then one link: the kernels
+    # files are independent TUs (host code in shuf_api.cu launches them through
+    # declarations in shuf_internal.cuh), so this equals the single-command build.
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", tmp, *sources()]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+    objdir = os.path.join(HERE, "build", f"obj{os.getpid()}")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *ARCH, *cflags, *extra, "-I", INCLUDE, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((subprocess.Popen(cmd), src))
+        objs.append(obj)
+    bad = [src for p, src in procs if p.wait() != 0]
+    if bad:
+        raise RuntimeError(f"nvcc failed on {bad}")
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs])
     os.replace(tmp, LIB)
+    shutil.rmtree(objdir, ignore_errors=True)
     return LIB
 
 

@@ -95,11 +95,14 @@ struct Leaf {
 };
 
 // Units of U leaves per warp: U = 32 (lane x owns leaf x of the unit) when
-// leaves are short, U = 1 when leaves of about L/2 or more already take the
-// warp-cooperative path -- then one long leaf per warp-unit spreads the long
-// leaves over all warps instead of 32 of them over one warp.
-__host__ __device__ inline uint32_t leaf_unit(uint32_t eb, uint32_t L) {
-    return 8u * ((L / 2u) * eb + 32u) > leaf_slot_bytes(eb, L) ? 1u : 32u;
+// leaves are short, U = 1 when a leaf of the launch's expected length `avg`
+// already takes the warp-cooperative path (fewer than 8 fit the slot) -- then
+// one long leaf per warp-unit spreads the long leaves over all warps instead
+// of 32 of them over one warp.  `avg` comes from the host: the expected child
+// length of the level (n / k^(l+1)) or the mean user-segment length.
+uint32_t leaf_unit(uint32_t eb, uint32_t L, uint64_t avg) {
+    if (avg > L) avg = L;
+    return 8u * ((uint32_t)avg * eb + 32u) > leaf_slot_bytes(eb, L) ? 1u : 32u;
 }
 
 // Leaf `lane` of unit u of a level's children: children U*g .. U*g+U-1 of
@@ -319,15 +322,15 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_children(RunParams rp, LevelParams lp) {
-    const uint32_t U = leaf_unit(EB, rp.L);
+    const uint32_t U = lp.leaf_unit;
     const ChildLeaves ls{&lp, rp.k, (rp.k + U - 1) / U, U};
     run_leaves<EB>(rp, lp.dst, ls, leaf_slot_bytes(EB, rp.L));
 }
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_segments(RunParams rp, const uint64_t* __restrict__ off,
-                                                                 uint64_t nsegs) {
-    const SegLeaves ls{off, nsegs, rp.seed, leaf_unit(EB, rp.L)};
+                                                                 uint64_t nsegs, uint32_t U) {
+    const SegLeaves ls{off, nsegs, rp.seed, U};
     run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
 }
 
@@ -377,7 +380,8 @@ cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cud
 
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
                                  cudaStream_t s, int grid) {
-    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments};
+    uint32_t U = leaf_unit(rp.eb, rp.L, num_segments ? rp.n / num_segments : 0);
+    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments, (void*)&U};
     return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L),
                             s);
 }

@@ -444,6 +444,7 @@ static LevelParams level_params(const ScratchLayout& l, unsigned char* sc, unsig
     unsigned char* buf1 = sc + l.pingpong;
     lp.src = (level & 1u) ? buf1 : buf0;
     lp.dst = (level & 1u) ? buf0 : buf1;
+    lp.leaf_unit = 32;
     return lp;
 }
 
@@ -554,7 +555,12 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     // (fork/join inside the call: still stream-ordered for the caller)
     const bool overlap = p->hist_overlap && !prof;
     for (uint32_t lv = 0; lv < G; ++lv) {
-        const LevelParams lp = level_params(lay, sc, buf0, lv);
+        LevelParams lp = level_params(lay, sc, buf0, lv);
+        {  // expected child length of the level: (n / segments) / k^(lv+1)
+            double avg = (double)p->n / (double)(d_offsets ? (nsegs ? nsegs : 1) : 1);
+            for (uint32_t i = 0; i <= lv; ++i) avg /= (double)p->k;
+            lp.leaf_unit = leaf_unit(p->eb, p->L, (uint64_t)avg);
+        }
         if (overlap && lv > 0) {
             if ((e = cudaStreamWaitEvent(st, p->ev_join, 0))) return cuda_fail(p, e);
         } else {

@@ -135,6 +135,7 @@ struct LevelParams {
     uint64_t max_segs, max_chunks;
     unsigned char* src;  // level input buffer
     unsigned char* dst;  // level output buffer
+    uint32_t leaf_unit;  // leaves per warp-unit of k_leaf_children (1 or 32, leaf_unit())
 };
 
 // ------------------------------------------------------- in-place mode ---
@@ -194,6 +195,7 @@ cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaS
 cudaError_t launch_finish_fast_ip(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
 cudaError_t configure_fast(uint32_t eb, uint32_t k);
 uint32_t fast_smem_bytes(uint32_t eb, uint32_t k);
+uint32_t leaf_unit(uint32_t eb, uint32_t L, uint64_t avg);
 cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
                                  cudaStream_t s, int grid);
