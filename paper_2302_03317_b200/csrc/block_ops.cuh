@@ -144,20 +144,30 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* Cw, uint32_t b, bool val
 // C holds nw packed-u16 counter tables of k entries (table w at C + w*kw,
 // kw = ceil(k/2) words).  Replace every count by its exclusive prefix in
 // (bucket, warp) order and write bucket starts to bst[0..k] (bst[k] = total).
-// Each thread owns a contiguous run of words.  All NT threads call.
+// With rix != nullptr also rix[b] = the number of non-empty buckets before b
+// (the run index of bucket b; the total must stay below 2^16: the two
+// prefixes share one scan).  Each thread owns a contiguous run of words.  All
+// NT threads call.
 template <int NT>
-__device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum) {
+__device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum,
+                                              uint32_t* rix = nullptr) {
     const uint32_t kw = (k + 1) >> 1;
     const uint32_t per = (kw + NT - 1) / NT;
     const uint32_t x0 = threadIdx.x * per, x1 = min(kw, x0 + per);
-    uint32_t mine = 0;
-    for (uint32_t x = x0; x < x1; ++x)
+    uint32_t mine = 0, ne = 0;
+    for (uint32_t x = x0; x < x1; ++x) {
+        uint32_t t0 = 0, t1 = 0;
         for (uint32_t w = 0; w < nw; ++w) {
             const uint32_t c = C[w * kw + x];
-            mine += (c & 0xFFFFu) + (c >> 16);
+            t0 += c & 0xFFFFu;
+            t1 += c >> 16;
         }
+        mine += t0 + t1;
+        ne += (t0 != 0) + (t1 != 0);
+    }
     uint32_t total;
-    uint32_t run = block_exclusive_sum<NT>(mine, wsum, &total);
+    const uint32_t pre = block_exclusive_sum<NT>(rix ? mine | (ne << 16) : mine, wsum, &total);
+    uint32_t run = rix ? pre & 0xFFFFu : pre, rr = pre >> 16;
     for (uint32_t x = x0; x < x1; ++x) {
         uint32_t t0 = 0, t1 = 0;
         for (uint32_t w = 0; w < nw; ++w) {
@@ -167,6 +177,12 @@ __device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t
         }
         bst[2 * x] = run;
         if (2 * x + 1 < k) bst[2 * x + 1] = run + t0;
+        if (rix) {
+            rix[2 * x] = rr;
+            rr += t0 != 0;
+            if (2 * x + 1 < k) rix[2 * x + 1] = rr;
+            rr += t1 != 0;
+        }
         uint32_t r0 = run, r1 = run + t0;
         for (uint32_t w = 0; w < nw; ++w) {
             const uint32_t c = C[w * kw + x];
@@ -176,30 +192,41 @@ __device__ __forceinline__ void scan_counters(uint32_t* C, uint32_t nw, uint32_t
         }
         run += t0 + t1;
     }
-    if (threadIdx.x == 0) bst[k] = total;
+    if (threadIdx.x == 0) bst[k] = rix ? total & 0xFFFFu : total;
     __syncthreads();
 }
 
 // As scan_counters for unpacked u32 counters: C holds nw tables of k words
 // (table w at C + w*k).
 template <int NT>
-__device__ __forceinline__ void scan_counters32(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum) {
+__device__ __forceinline__ void scan_counters32(uint32_t* C, uint32_t nw, uint32_t k, uint32_t* bst, uint32_t* wsum,
+                                                uint32_t* rix = nullptr) {
     const uint32_t per = (k + NT - 1) / NT;
     const uint32_t x0 = threadIdx.x * per, x1 = min(k, x0 + per);
-    uint32_t mine = 0;
-    for (uint32_t x = x0; x < x1; ++x)
-        for (uint32_t w = 0; w < nw; ++w) mine += C[w * k + x];
+    uint32_t mine = 0, ne = 0;
+    for (uint32_t x = x0; x < x1; ++x) {
+        uint32_t c = 0;
+        for (uint32_t w = 0; w < nw; ++w) c += C[w * k + x];
+        mine += c;
+        ne += c != 0;
+    }
     uint32_t total;
-    uint32_t run = block_exclusive_sum<NT>(mine, wsum, &total);
+    const uint32_t pre = block_exclusive_sum<NT>(rix ? mine | (ne << 16) : mine, wsum, &total);
+    uint32_t run = rix ? pre & 0xFFFFu : pre, rr = pre >> 16;
     for (uint32_t x = x0; x < x1; ++x) {
         bst[x] = run;
+        const uint32_t r0 = run;
         for (uint32_t w = 0; w < nw; ++w) {
             const uint32_t c = C[w * k + x];
             C[w * k + x] = run;
             run += c;
         }
+        if (rix) {
+            rix[x] = rr;
+            rr += run != r0;
+        }
     }
-    if (threadIdx.x == 0) bst[k] = total;
+    if (threadIdx.x == 0) bst[k] = rix ? total & 0xFFFFu : total;
     __syncthreads();
 }
 

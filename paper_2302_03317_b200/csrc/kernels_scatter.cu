@@ -13,13 +13,20 @@
 //
 //   B(t)   scan: (bucket, warp)-major exclusive prefix of the counts -> per-
 //          warp slot bases, tile bucket starts, run destinations delta
+//          and the run map of the sorted tile: the non-empty buckets in order
+//          are runs 0, 1, ..; rdelta[r] = destination minus slot of run r;
+//          winfo[w] = (bit i set iff slot 32w+i starts a run) | (number of
+//          runs started before slot 32w) << 32
 //   C(t)   rank + place: each round reads 32 draws and 32 elements of the raw
 //          tile, takes every element's slot with one ordered shared atomic on
 //          the warp's table (whose entries the scan set to the warp's first
-//          slot per bucket) and stores element and bucket at that slot
+//          slot per bucket) and stores the element at that slot
 //   ---- barrier: raw tile consumed -> bulk load of tile t+1 into it
-//   D(t)   copy-out: slot x -> dst[delta[bucket(x)] + x]; consecutive lanes
-//          take consecutive slots, i.e. whole bucket runs (coalesced)
+//   D(t)   copy-out: window w of 32 slots, slot x = 32w + lane ->
+//          dst[rdelta[run(x)] + x], run(x) = winfo.base + popc(winfo.bits &
+//          lanemask_le) - 1: one broadcast load per window instead of a
+//          bucket byte stored per slot; consecutive lanes take consecutive
+//          slots, i.e. whole bucket runs (coalesced)
 //   A(t+1) draws + counts of the next tile (D4 Philox: positions only, no
 //          data): lane-owned Philox groups -> draw buffer, per-warp counts
 //   ---- barrier
@@ -57,7 +64,7 @@ struct SCfg {
 };
 
 struct SLayout {
-    uint32_t raw, sorted, draws, slotb, tab, bst, run, delta, wsum, bar, total;
+    uint32_t raw, sorted, draws, tab, bst, rix, winfo, run, delta, wsum, bar, total;
 };
 
 template <int EB, bool NARROW>
@@ -73,12 +80,13 @@ __host__ __device__ inline SLayout s_layout(uint32_t k) {
     L.raw = take(C::T * EB + 16);
     L.sorted = take(C::T * EB);
     L.draws = take((C::T / C::dpg + 2) * 16);
-    L.slotb = take((NARROW ? 1u : 2u) * C::T);             // bucket of every slot (u8 / u16)
     L.tab = take(C::NW * (C::P16 ? (k + 1) / 2 : k) * 4);  // u32 counters or packed u16 pairs
     L.bst = take((k + 1) * 4);
+    L.rix = take(k * 4);             // run index of every bucket
+    L.winfo = take(C::T / 32 * 8);   // per 32-slot window: run-start bits | runs before << 32
     L.run = take(k * 8);
-    L.delta = take(k * 8);  // destination minus slot: u32 relative to the segment start (mod 2^32),
-                            // u64 absolute for segments longer than 2^32 elements
+    L.delta = take(k * 8);  // per run: destination minus slot, u32 relative to the segment start
+                            // (mod 2^32), u64 absolute for segments longer than 2^32 elements
     L.wsum = take((C::NW + 1) * 4);
     L.bar = take(16);
     L.total = off;
@@ -213,8 +221,8 @@ __device__ __forceinline__ void s_draw_count(const BucketParams& bp, PhiloxKey k
 // C: rank + place of warp w's rounds.  FULL: cnt == T (no checks).
 template <int EB, bool NARROW, bool ORD, bool FULL>
 __device__ __forceinline__ void s_place(const unsigned char* raw, uint64_t q0, const unsigned char* draws,
-                                        uint32_t doff, uint32_t cnt, unsigned char* sorted, unsigned char* slotb_,
-                                        uint32_t* Tw, uint32_t warp, uint32_t lane, uint32_t* err) {
+                                        uint32_t doff, uint32_t cnt, unsigned char* sorted, uint32_t* Tw,
+                                        uint32_t warp, uint32_t lane, uint32_t* err) {
     using E = typename ElemT<EB>::type;
     using D = typename std::conditional<NARROW, unsigned char, uint16_t>::type;
     using C = SCfg<EB, NARROW>;
@@ -222,7 +230,6 @@ __device__ __forceinline__ void s_place(const unsigned char* raw, uint64_t q0, c
     const E* el = reinterpret_cast<const E*>(raw + ((q0 * EB) & 15u)) + e0 + lane;
     const D* dp = reinterpret_cast<const D*>(draws) + doff + e0 + lane;
     E* so = reinterpret_cast<E*>(sorted);
-    D* sb = reinterpret_cast<D*>(slotb_);
     const int32_t wrem = (int32_t)cnt - (int32_t)e0;  // elements of this warp's range in the tile
 #pragma unroll
     for (uint32_t r = 0; r < C::R; ++r) {
@@ -249,10 +256,7 @@ __device__ __forceinline__ void s_place(const unsigned char* raw, uint64_t q0, c
             slot = warp_rank(Tw, b, valid, false);
         }
         if (ORD && r == 0 && warp == 0) check_rank_order(b, valid, slot, err);
-        if (valid) {
-            so[slot] = v;
-            sb[slot] = (D)b;
-        }
+        if (valid) so[slot] = v;
     }
 }
 
@@ -269,7 +273,8 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW>::NT, SCfg<EB, NARROW>::MINB)
     unsigned char* raw = sm + Ly.raw;
     unsigned char* sorted = sm + Ly.sorted;
     unsigned char* draws = sm + Ly.draws;
-    unsigned char* slotb = sm + Ly.slotb;
+    uint32_t* rix = reinterpret_cast<uint32_t*>(sm + Ly.rix);
+    uint64_t* winfo = reinterpret_cast<uint64_t*>(sm + Ly.winfo);
     uint32_t* tab = reinterpret_cast<uint32_t*>(sm + Ly.tab);
     uint32_t* bst = reinterpret_cast<uint32_t*>(sm + Ly.bst);
     uint64_t* running = reinterpret_cast<uint64_t*>(sm + Ly.run);
@@ -309,28 +314,35 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW>::NT, SCfg<EB, NARROW>::MINB)
             for (uint32_t b = tid; b < k; b += NT)
                 running[b] = sg.start + lp.prefix[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] - base0;
         }
-        if (!C::P16) scan_counters32<NT>(tab, C::NW, k, bst, wsum);
-        else scan_counters<NT>(tab, C::NW, k, bst, wsum);
+        for (uint32_t w = tid; w < T / 32; w += NT) winfo[w] = 0;  // ordered before the run bits by the scan's barriers
+        if (!C::P16) scan_counters32<NT>(tab, C::NW, k, bst, wsum, rix);
+        else scan_counters<NT>(tab, C::NW, k, bst, wsum, rix);
         // a segment of <= 2^32 elements: every destination minus the segment
         // start fits 32 bits, so delta is kept modulo 2^32 (half the lookup
         // bytes in the copy-out); longer segments keep 64-bit deltas
         const bool wide = (sg.len >> 32) != 0 || (rp.dbg & 64u);  // SHUF_DBG=64: test hook forcing the 64-bit path
         for (uint32_t b = tid; b < k; b += NT) {
-            if (wide) delta64[b] = running[b] - bst[b];
-            else delta[b] = (uint32_t)(running[b] - sg.start) - bst[b];
-            running[b] += bst[b + 1] - bst[b];
+            const uint32_t s0 = bst[b], s1 = bst[b + 1];
+            if (s1 > s0) {  // run r = rix[b]: slots [s0, s1)
+                const uint32_t r = rix[b];
+                if (wide) delta64[r] = running[b] - s0;
+                else delta[r] = (uint32_t)(running[b] - sg.start) - s0;
+                atomicOr(reinterpret_cast<uint32_t*>(&winfo[s0 >> 5]), 1u << (s0 & 31u));
+                // windows whose first slot lies in the run
+                for (uint32_t w = (s0 + 31u) >> 5; (w << 5) < s1; ++w)
+                    reinterpret_cast<uint32_t*>(&winfo[w])[1] = r + ((w << 5) == s0 ? 0u : 1u);
+                running[b] += s1 - s0;
+            }
         }
         // ---- C: rank + place (the tile's data must have landed)
         mbar_wait(&bar[0], ph);
         ph ^= 1u;
         const uint32_t doff = (uint32_t)((cur.q0 - sg.origin) & (C::dpg - 1));
         if (cnt == T)
-            s_place<EB, NARROW, ORD, true>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
-                                           &rp.hdr->error);
+            s_place<EB, NARROW, ORD, true>(raw, cur.q0, draws, doff, cnt, sorted, Tw, warp, lane, &rp.hdr->error);
         else
-            s_place<EB, NARROW, ORD, false>(raw, cur.q0, draws, doff, cnt, sorted, slotb, Tw, warp, lane,
-                                            &rp.hdr->error);
-        __syncthreads();  // raw consumed; sorted, slotb and delta complete
+            s_place<EB, NARROW, ORD, false>(raw, cur.q0, draws, doff, cnt, sorted, Tw, warp, lane, &rp.hdr->error);
+        __syncthreads();  // raw consumed; sorted, run map and delta complete
         // ---- next tile of this CTA's sequence: load it into the raw buffer
         STile nxt = cur;
         nxt.q0 = cur.q0 + cnt;
@@ -341,24 +353,34 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW>::NT, SCfg<EB, NARROW>::MINB)
         }
         const uint32_t ncnt = (uint32_t)min((uint64_t)T, nxt.q1 - nxt.q0);
         if (nxt.chunk < nchunk) s_issue_load<EB>(nxt.q0, ncnt, src, raw, &bar[0]);
-        // ---- D: copy-out of tile `cur`: slot x -> dst[delta[bucket(x)] + x]
+        // ---- D: copy-out of tile `cur`: slot x -> dst[delta[run(x)] + x]
         {
             const E* so = reinterpret_cast<const E*>(sorted);
-            const D* sb = reinterpret_cast<const D*>(slotb);
+            const uint32_t le = lanemask_le();
             if (!wide) {
                 E* dst = reinterpret_cast<E*>(dstb) + sg.start;
                 if (cnt == T) {
-#pragma unroll
+#pragma unroll 8
                     for (uint32_t j = 0; j < T / NT; ++j) {
                         const uint32_t x = tid + j * NT;
-                        dst[(uint32_t)(delta[sb[x]] + x)] = so[x];
+                        const uint64_t wi = winfo[x >> 5];
+                        const uint32_t r = (uint32_t)(wi >> 32) + __popc((uint32_t)wi & le) - 1u;
+                        dst[(uint32_t)(delta[r] + x)] = so[x];
                     }
                 } else {
-                    for (uint32_t x = tid; x < cnt; x += NT) dst[(uint32_t)(delta[sb[x]] + x)] = so[x];
+                    for (uint32_t x = tid; x < ((cnt + 31u) & ~31u); x += NT) {
+                        const uint64_t wi = winfo[x >> 5];
+                        const uint32_t r = (uint32_t)(wi >> 32) + __popc((uint32_t)wi & le) - 1u;
+                        if (x < cnt) dst[(uint32_t)(delta[r] + x)] = so[x];
+                    }
                 }
             } else {
                 E* dst = reinterpret_cast<E*>(dstb);
-                for (uint32_t x = tid; x < cnt; x += NT) dst[delta64[sb[x]] + x] = so[x];
+                for (uint32_t x = tid; x < ((cnt + 31u) & ~31u); x += NT) {
+                    const uint64_t wi = winfo[x >> 5];
+                    const uint32_t r = (uint32_t)(wi >> 32) + __popc((uint32_t)wi & le) - 1u;
+                    if (x < cnt) dst[delta64[r] + x] = so[x];
+                }
             }
         }
         if (nxt.chunk >= nchunk) break;
@@ -366,7 +388,7 @@ __global__ void __launch_bounds__(SCfg<EB, NARROW>::NT, SCfg<EB, NARROW>::MINB)
         const SegDesc nsg = next_chunk ? lp.segs[nxt.seg] : sg;
         s_draw_count<EB, NARROW>(bp, make_key(nsg.key), lp.level, nxt.q0 - nsg.origin, ncnt, draws, Tw, kw, warp,
                                  lane);
-        __syncthreads();  // copy-out done (sorted, slotb, delta free); counts complete
+        __syncthreads();  // copy-out done (sorted, run map, delta free); counts complete
         new_chunk = next_chunk;
         cur = nxt;
         cnt = ncnt;
