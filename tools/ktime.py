@@ -70,7 +70,7 @@ if "--scatter" in sys.argv:
         nx = c[256 + (it + 1) * 6]
         print(f"  tile {it}: {t[1]-t[0]:6d} {t[2]-t[1]:6d} {t[3]-t[2]:6d} {t[4]-t[3]:6d} {t[5]-t[4]:6d}  total {nx - t[0] if nx else 0:6d}")
     sys.exit(0)
-if os.environ.get("SHUF_DBG") == "4":
+if int(os.environ.get("SHUF_DBG", "0")) & 4:
     print("pipelined finish CTA 0 per item (cycles): S count+scan, S place, S period; F FY, F period")
     for it in range(1, 30):
         t = c[it * 6: it * 6 + 5]
