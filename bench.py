@@ -267,7 +267,7 @@ def main():
     eff_gbps = eff_bytes / (ms / 1e3) / 1e9
 
     # ---- per-kernel breakdown (separate pass; every launch bracketed by events on `stream`)
-    if inplace:  # the in-place mode synchronises per level: no per-kernel split, the step is the unit
+    if inplace:  # the in-place mode is one launch of a device-driven CUDA graph: no per-kernel split, the step is the unit
         prof = {c: (0.0, 0) for c in shuf.KERNEL_CLASSES}
         prof["scatter"] = (ms, 1)
     else:
@@ -370,7 +370,9 @@ def main():
                        "l2": "inputs larger than L2 (no flush)" if w.n * w.elem_bytes > (256 << 20)
                        else "input fits in L2: not an HBM figure",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "mode": args.mode},
+                       "mode": args.mode,
+                       "aux_bytes": int(scratch.numel()) if inplace else None,
+                       "scratch_bytes": None if inplace else int(scratch.numel())},
             "eff_GBps": eff_gbps, "frac_of_8TBps": eff_gbps / SPEC_HBM_GBPS,
             "frac_of_measured_copy": eff_gbps / hbm_peak, "effective_bytes_per_step": eff_bytes,
             "elements_scattered_per_step": scattered, "levels": {"hbm": stats["scattered_hbm"],

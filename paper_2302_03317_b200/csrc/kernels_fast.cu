@@ -696,6 +696,7 @@ __global__ void __launch_bounds__(XNT, 1) k_finish_fast(RunParams rp, LevelParam
 // Children of an in-place level batch (kernels_inplace.cu), in place in ptr.
 template <int EB, bool NARROW, bool ORD>
 __global__ void __launch_bounds__(XNT, 1) k_finish_fast_ip(RunParams rp, IpParams ip) {
+    ip = ip_resolve(ip);
     XSrc xs;
     xs.lp = nullptr;
     xs.ip = &ip;

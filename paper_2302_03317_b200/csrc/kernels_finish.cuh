@@ -622,6 +622,7 @@ struct IpChildIter {
 
 template <int EB, bool NARROW, bool ORD>
 __global__ void __launch_bounds__(NTF, 1) k_finish_ipchildren(RunParams rp, IpParams ip) {
+    ip = ip_resolve(ip);
     const uint32_t groups = (rp.k + kUnit - 1) / kUnit;
     const uint64_t units = (uint64_t)ip.nseg * groups;
     if (blockIdx.x >= units) return;

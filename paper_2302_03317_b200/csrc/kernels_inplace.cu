@@ -106,6 +106,7 @@ __device__ __forceinline__ void scan_k(const uint32_t* in, uint32_t* out, uint32
 // ------------------------------------------------------------------ P0 ----
 // One CTA: stripe counts and bases of the batch's segments, stripe -> segment.
 __global__ void __launch_bounds__(256) k_ip_stripes(IpParams ip) {
+    ip = ip_resolve(ip);
     __shared__ uint32_t wsum[256 / 32 + 1];
     uint32_t base = 0;
     for (uint32_t s0 = 0; s0 < ip.nseg; s0 += 256) {
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(256) k_ip_stripes(IpParams ip) {
 // ------------------------------------------------------------------ P1 ----
 template <int EB>
 __global__ void __launch_bounds__(kIpThreads) k_ip_classify(RunParams rp, IpParams ip) {
+    ip = ip_resolve(ip);
     using E = typename ElemT<EB>::type;
     constexpr uint32_t B = IpCfg<EB>::B, T = IpCfg<EB>::T, R = IpCfg<EB>::R;
     const uint32_t tid = threadIdx.x, k = rp.k;
@@ -230,11 +232,14 @@ __global__ void __launch_bounds__(kIpThreads) k_ip_classify(RunParams rp, IpPara
 }
 
 // ---------------------------------------------------------------- plan ----
-// CTA per batch segment: S[s][0..k] (segment-relative bucket starts), and the
-// (write, read) pointers of every bucket's block region.
+// CTA per batch segment (grid-stride): S[s][0..k] (segment-relative bucket
+// starts), and the (write, read) pointers of every bucket's block region.
 __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint32_t B) {
+    ip = ip_resolve(ip);
     __shared__ unsigned long long wsum[256 / 32 + 1];
-    const uint32_t s = blockIdx.x, k = rp.k, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    __shared__ uint32_t work[kMaxK];
+    const uint32_t k = rp.k, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    for (uint32_t s = blockIdx.x; s < ip.nseg; s += gridDim.x) {
     const IpSeg sg = ip.segs[s];
     const uint64_t* N = ip.N + (uint64_t)s * k;
     uint64_t* S = ip.S + (uint64_t)s * (k + 1);
@@ -271,7 +276,6 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
     }
     __syncthreads();
     const uint64_t nfb = sg.len / B;
-    __shared__ uint32_t work[kMaxK];
     for (uint32_t d = tid; d < k; d += 256) {
         const uint64_t w = (S[d] + B - 1) / B;
         const uint64_t re = min((S[d + 1] + B - 1) / B, nfb);
@@ -288,6 +292,8 @@ __global__ void __launch_bounds__(256) k_ip_plan(RunParams rp, IpParams ip, uint
         }
         ip.segtot[s] = run;
     }
+    __syncthreads();
+    }
 }
 
 // ------------------------------------------------------------------ P2 ----
@@ -300,6 +306,7 @@ constexpr uint32_t kIpPermSmem = (kIpPermThreads / 32) * 32 * kIpBlockBytes + (k
 
 template <int EB>
 __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpParams ip) {
+    ip = ip_resolve(ip);
     constexpr uint32_t B = IpCfg<EB>::B;
     constexpr uint32_t W = kIpBlockBytes / 4;  // 32 words per block
     const uint32_t k = rp.k, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -470,6 +477,7 @@ __global__ void __launch_bounds__(kIpPermThreads) k_ip_permute(RunParams rp, IpP
 // the stripes' partial buffers; queue children longer than S_fuse.
 template <int EB>
 __global__ void __launch_bounds__(256) k_ip_fill(RunParams rp, IpParams ip) {
+    ip = ip_resolve(ip);
     using E = typename ElemT<EB>::type;
     constexpr uint32_t B = IpCfg<EB>::B;
     const uint32_t k = rp.k, lane = threadIdx.x & 31u;
@@ -516,6 +524,133 @@ __global__ void __launch_bounds__(256) k_ip_fill(RunParams rp, IpParams ip) {
     }
 }
 
+// ------------------------------------------------ device-driven loop ----
+// The level loop of the in-place mode runs on the device (shuf_api.cu builds a
+// CUDA graph: WHILE(levels){ k_ip_level_plan; WHILE(batches){ batch kernels;
+// k_ip_batch_next }; k_ip_level_next }).  No host round trip per level.
+
+// Level 0: the root segment, loop state.
+__global__ void k_ip_init(IpParams ip, Header* hdr, uint64_t n, IpState init) {
+    hdr->root_off[0] = 0;
+    hdr->root_off[1] = n;
+    ip.segbase[0][0] = IpSeg{0, n, 0u, 0u};
+    IpState* st = ip.state;
+    *st = init;
+    st->level = 0;
+    st->cur = 0;
+    st->batch = 0;
+    st->nbatch = 0;
+    st->nseg = 1;
+}
+
+// Cut the level's segment list into batches: with P_s the exclusive prefix of
+// the segments' stripe counts, segment s goes to batch floor(P_s / C).  A
+// segment has at most C stripes (shuf_api.cu chooses Z so), so a batch holds
+// fewer than 2C <= cap stripes and segments; batch indices a long segment
+// jumps over stay empty (their kernels return at once).
+__global__ void __launch_bounds__(1024) k_ip_level_plan(RunParams rp, IpParams ip, cudaGraphConditionalHandle hb) {
+    __shared__ uint32_t wsum[1024 / 32 + 1];
+    __shared__ unsigned long long tot;
+    IpState* st = ip.state;
+    const uint32_t cur = st->cur, tid = threadIdx.x;
+    const IpSeg* segs = ip.segbase[cur];
+    uint32_t nseg = st->level == 0 ? 1u : ip.nnext_base[cur];
+    if (nseg > ip.max_next) {  // list overflow (cannot happen with the planned capacity)
+        if (tid == 0) atomicCAS(&rp.hdr->error, 0u, 7u);
+        nseg = 0;
+    }
+    const uint32_t C = st->C;
+    // total stripes -> number of batches
+    if (tid == 0) tot = 0;
+    __syncthreads();
+    unsigned long long mine = 0;
+    for (uint32_t x = tid; x < nseg; x += 1024) mine += (segs[x].len + ip.Z - 1) / ip.Z;
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+    if ((tid & 31u) == 0 && mine) atomicAdd(&tot, mine);
+    __syncthreads();
+    uint32_t nb = (uint32_t)((tot + C - 1) / C);
+    if (nb > st->max_batches) {
+        if (tid == 0) atomicCAS(&rp.hdr->error, 0u, 7u);
+        nb = 0;
+        nseg = 0;
+    }
+    for (uint32_t b = tid; b < nb; b += 1024) st->batches[b] = IpBatch{0u, 0u, 0u, 0xFFFFFFFFu};
+    __syncthreads();
+    uint32_t base = 0;
+    for (uint32_t s0 = 0; s0 < nseg; s0 += 1024) {
+        const uint32_t s = s0 + tid;
+        const uint32_t nz = s < nseg ? (uint32_t)((segs[s].len + ip.Z - 1) / ip.Z) : 0u;
+        uint32_t total;
+        const uint32_t ex = block_exclusive_sum<1024>(nz, wsum, &total);
+        if (s < nseg) {
+            const uint32_t b = (base + ex) / C;
+            atomicMin(&st->batches[b].first, s);
+            atomicAdd(&st->batches[b].nz, nz);
+        }
+        base += total;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t nxt = nseg;
+        for (int32_t b = (int32_t)nb - 1; b >= 0; --b) {
+            IpBatch& bt = st->batches[b];
+            if (bt.first == 0xFFFFFFFFu) {
+                bt.s0 = nxt;
+                bt.nseg = 0;
+            } else {
+                bt.s0 = bt.first;
+                bt.nseg = nxt - bt.first;
+                nxt = bt.first;
+            }
+        }
+        st->nbatch = nb;
+        st->batch = 0;
+        st->nseg = nseg;
+        ip.nnext_base[cur ^ 1u] = 0;
+        *ip.cursor = 0;
+        cudaGraphSetConditional(hb, nb > 0 ? 1u : 0u);
+    }
+}
+
+__global__ void k_ip_batch_next(IpParams ip, cudaGraphConditionalHandle hb) {
+    IpState* st = ip.state;
+    const uint32_t b = ++st->batch;
+    *ip.cursor = 0;
+    cudaGraphSetConditional(hb, b < st->nbatch ? 1u : 0u);
+}
+
+__global__ void k_ip_level_next(RunParams rp, IpParams ip, cudaGraphConditionalHandle hl) {
+    IpState* st = ip.state;
+    const uint32_t nn = ip.nnext_base[st->cur ^ 1u];
+    st->cur ^= 1u;
+    st->level += 1;
+    bool more = nn > 0;
+    if (more && st->level >= kMaxLevels) {
+        atomicCAS(&rp.hdr->error, 0u, 5u);  // SHUF_ERR_DEPTH
+        more = false;
+    }
+    cudaGraphSetConditional(hl, more ? 1u : 0u);
+}
+
+cudaError_t launch_ip_init(const IpParams& ip, Header* hdr, uint64_t n, const IpState& init, cudaStream_t s) {
+    k_ip_init<<<1, 1, 0, s>>>(ip, hdr, n, init);
+    return cudaGetLastError();
+}
+cudaError_t launch_ip_level_plan(const RunParams& rp, const IpParams& ip, cudaGraphConditionalHandle hb,
+                                 cudaStream_t s) {
+    k_ip_level_plan<<<1, 1024, 0, s>>>(rp, ip, hb);
+    return cudaGetLastError();
+}
+cudaError_t launch_ip_batch_next(const IpParams& ip, cudaGraphConditionalHandle hb, cudaStream_t s) {
+    k_ip_batch_next<<<1, 1, 0, s>>>(ip, hb);
+    return cudaGetLastError();
+}
+cudaError_t launch_ip_level_next(const RunParams& rp, const IpParams& ip, cudaGraphConditionalHandle hl,
+                                 cudaStream_t s) {
+    k_ip_level_next<<<1, 1, 0, s>>>(rp, ip, hl);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- dispatch ---
 __global__ void k_ip_root(Header* hdr, uint64_t n) {
     hdr->root_off[0] = 0;
@@ -556,12 +691,12 @@ cudaError_t launch_ip_stripes(const IpParams& ip, cudaStream_t s) {
 
 cudaError_t launch_ip_classify(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp, (void*)&ip};
-    const int g = (int)min((uint64_t)grid, (uint64_t)ip.nstripes);
+    const int g = ip.state ? grid : (int)min((uint64_t)grid, (uint64_t)ip.nstripes);  // device-resolved batch: any size
     return cudaLaunchKernel(ip_fn(rp.eb, 0), dim3(g), dim3(kIpThreads), args, ip_classify_smem_bytes(rp.eb, rp.k), s);
 }
 
 cudaError_t launch_ip_plan(const RunParams& rp, const IpParams& ip, cudaStream_t s) {
-    k_ip_plan<<<ip.nseg, 256, 0, s>>>(rp, ip, kIpBlockBytes / rp.eb);
+    k_ip_plan<<<ip.state ? kIpBatchCap : ip.nseg, 256, 0, s>>>(rp, ip, kIpBlockBytes / rp.eb);
     return cudaGetLastError();
 }
 
@@ -573,7 +708,7 @@ cudaError_t launch_ip_permute(const RunParams& rp, const IpParams& ip, cudaStrea
 cudaError_t launch_ip_fill(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp, (void*)&ip};
     const uint64_t warps = (uint64_t)ip.nseg * rp.k;
-    const int g = (int)min((uint64_t)grid, (warps + 7) / 8);
+    const int g = ip.state ? grid : (int)min((uint64_t)grid, (warps + 7) / 8);
     return cudaLaunchKernel(ip_fn(rp.eb, 2), dim3(g), dim3(256), args, 0, s);
 }
 

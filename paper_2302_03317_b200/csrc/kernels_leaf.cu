@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_items(RunParams rp) {
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_ipchildren(RunParams rp, IpParams ip) {
+    ip = ip_resolve(ip);
     const IpChildLeaves ls{&ip, rp.k, (rp.k + 31) / 32, rp.seed};
     run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
 }

@@ -20,9 +20,10 @@ using namespace shuf;
 
 // Byte offsets of the in-place mode's auxiliary buffer (kernels_inplace.cu).
 struct IpAuxLayout {
-    uint64_t header, ctr, segs[2], zseg, N, F, S, wr, regpre, segtot, ovf, ovfd, pcnt, part, tags, flags, total;
-    uint64_t Z, max_segs;
-    uint32_t cap;
+    uint64_t header, ctr, state, batches, segs[2], zseg, N, F, S, wr, regpre, segtot, ovf, ovfd, pcnt, part, tags, flags,
+        total;
+    uint64_t Z, max_segs, max_batches;
+    uint32_t cap, C;
 };
 
 struct shuf_plan_s {
@@ -43,6 +44,14 @@ struct shuf_plan_s {
     cudaEvent_t ev_fork, ev_join;
     bool ip_ready;
     int grid_ipc, grid_ipp;
+    // in-place mode: the device-driven level loop as an instantiated CUDA graph,
+    // cached for the (ptr, aux, max_levels, run_leaves) it was built for
+    cudaGraphExec_t ip_exec;
+    cudaStream_t ip_cap_stream;
+    void *ip_ptr, *ip_aux;
+    uint32_t ip_maxlv;
+    int ip_leaves;
+    uint64_t ip_nodes;
     int rank_ordered;
     uint32_t finish_smem, scatter_smem;
     int last_cuda_error;
@@ -187,23 +196,27 @@ static ScratchLayout compute_layout(const shuf_plan_s* p, uint64_t segs0, bool s
     return l;
 }
 
-// In-place aux: batches of <= cap stripes / segments; stripes of Z elements
-// (a multiple of the block and of the classify tile) so that one segment
-// never needs more than cap stripes.
+// In-place aux: batches of < 2C <= cap stripes / segments; stripes of Z
+// elements (a multiple of the block and of the classify tile) chosen so that
+// one segment never has more than C stripes (k_ip_level_plan).
 static void compute_ip_layout(shuf_plan_s* p) {
     IpAuxLayout& l = p->ipl;
     const uint64_t n = p->n, k = p->k;
     const uint64_t B = kIpBlockBytes / p->eb;
     // batch capacity: the per-(stripe|segment, bucket) buffers (~2 blocks + 32 B each) stay within
-    // ~4 % of the data plus 32 MiB, and between 64 and kIpBatchCap entries
+    // ~2.5 % of the data plus 16 MiB, and between 64 and kIpBatchCap entries (aux total < 5 % of the data
+    // above 1 GiB, tests/test_library_cpu.py)
     const uint64_t per = k * (2 * kIpBlockBytes + 32);
-    uint64_t capb = (n * p->eb / 25 + (32ull << 20)) / per;
+    uint64_t capb = (n * p->eb / 40 + (16ull << 20)) / per;
     capb = capb < 64 ? 64 : (capb > kIpBatchCap ? kIpBatchCap : capb);
-    l.Z = align_up((n + capb - 1) / capb, 4096);
+    l.C = (uint32_t)(capb / 2);
+    l.Z = align_up((n + l.C - 1) / l.C, 4096);
     if (l.Z < 65536) l.Z = 65536;
     l.max_segs = n / ((uint64_t)p->S_fuse + 1) + 1;
     uint64_t cap = n / l.Z + l.max_segs + 1;
     l.cap = (uint32_t)(cap < capb ? cap : capb);
+    if (l.cap < l.C) l.C = l.cap;
+    l.max_batches = (n / l.Z + l.max_segs + 1) / l.C + 2;
     uint64_t off = 0;
     auto take = [&off](uint64_t bytes) {
         const uint64_t at = off;
@@ -212,6 +225,8 @@ static void compute_ip_layout(shuf_plan_s* p) {
     };
     l.header = take(sizeof(Header));
     l.ctr = take(sizeof(IpCounters));
+    l.state = take(sizeof(IpState));
+    l.batches = take(l.max_batches * sizeof(IpBatch));
     l.segs[0] = take(l.max_segs * sizeof(IpSeg));
     l.segs[1] = take(l.max_segs * sizeof(IpSeg));
     l.zseg = take((uint64_t)l.cap * 4);
@@ -603,9 +618,10 @@ extern "C" shuf_status shuf_aux_bytes_inplace(shuf_plan_t p, uint64_t* bytes) {
     return SHUF_OK;
 }
 
-// Host-orchestrated level loop of the in-place mode: one stream
-// synchronisation per level (the next level's segment list is read back to
-// cut it into batches of <= cap stripes).
+// The in-place mode: its level loop runs on the device -- one launch of a
+// cached CUDA graph whose two nested WHILE nodes (levels, batches) are driven
+// by k_ip_level_plan / k_ip_batch_next / k_ip_level_next; no host
+// synchronisation and no host round trip per level.
 static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStream_t st, uint32_t max_levels,
                                    int run_leaves) {
     p->last_launches = 0;
@@ -657,82 +673,134 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
     rp.dbg = 0;
     uint64_t launches = 0;
     Prof* prof = nullptr;
-    if ((e = cudaMemsetAsync(ax, 0, l.segs[0], st))) return cuda_fail(p, e);  // header + counters
-    if ((e = cudaMemsetAsync(ax + l.N, 0, l.S - l.N, st))) return cuda_fail(p, e);  // N, F
-    if ((e = cudaMemsetAsync(ax + l.ovf, 0, l.ovfd - l.ovf, st))) return cuda_fail(p, e);
-    LAUNCH(SHUF_K_INIT, launch_ip_root(hdr, p->n, st));
-    if (p->n <= p->S_fuse) {
-        if (p->n <= p->L) LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, hdr->root_off, 1, st, 1));
-        else LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
-        p->last_launches = launches;
-        return SHUF_OK;
-    }
-    if (max_levels == 0) {
-        p->last_launches = launches;
-        return SHUF_OK;
-    }
-    IpSeg root{0, p->n, 0, 0};
-    IpSeg* segs[2] = {reinterpret_cast<IpSeg*>(ax + l.segs[0]), reinterpret_cast<IpSeg*>(ax + l.segs[1])};
-    if ((e = cudaMemcpyAsync(segs[0], &root, sizeof root, cudaMemcpyHostToDevice, st))) return cuda_fail(p, e);
-    uint32_t nseg = 1, cur = 0;
-    std::vector<IpSeg> hs;
-    for (uint32_t lv = 0; nseg > 0; ++lv) {
-        if (lv >= kMaxLevels) return SHUF_ERR_DEPTH;
-        hs.resize(nseg);
-        if ((e = cudaMemcpyAsync(hs.data(), segs[cur], nseg * sizeof(IpSeg), cudaMemcpyDeviceToHost, st)))
-            return cuda_fail(p, e);
-        if ((e = cudaMemsetAsync(&ctr->nnext[cur ^ 1u], 0, 4, st))) return cuda_fail(p, e);
-        if ((e = cudaStreamSynchronize(st))) return cuda_fail(p, e);
-        for (uint32_t s0 = 0; s0 < nseg;) {
-            uint32_t s1 = s0, nz = 0;
-            while (s1 < nseg && s1 - s0 < l.cap) {
-                const uint32_t z = (uint32_t)((hs[s1].len + l.Z - 1) / l.Z);
-                if (s1 > s0 && nz + z > l.cap) break;
-                nz += z;
-                ++s1;
-            }
-            IpParams ip;
-            ip.segs = segs[cur] + s0;
-            ip.nseg = s1 - s0;
-            ip.nstripes = nz;
-            ip.level = lv;
-            ip.pad = 0;
-            ip.Z = l.Z;
-            ip.zseg = reinterpret_cast<uint32_t*>(ax + l.zseg);
-            ip.N = reinterpret_cast<uint64_t*>(ax + l.N);
-            ip.F = reinterpret_cast<uint32_t*>(ax + l.F);
-            ip.S = reinterpret_cast<uint64_t*>(ax + l.S);
-            ip.wr = reinterpret_cast<uint64_t*>(ax + l.wr);
-            ip.regpre = reinterpret_cast<uint32_t*>(ax + l.regpre);
-            ip.segtot = reinterpret_cast<uint64_t*>(ax + l.segtot);
-            ip.ovf = reinterpret_cast<uint32_t*>(ax + l.ovf);
-            ip.ovfd = ax + l.ovfd;
-            ip.pcnt = reinterpret_cast<uint32_t*>(ax + l.pcnt);
-            ip.part = ax + l.part;
-            ip.tags = reinterpret_cast<uint16_t*>(ax + l.tags);
-            ip.next = segs[cur ^ 1u];
-            ip.nnext = &ctr->nnext[cur ^ 1u];
-            ip.max_next = l.max_segs;
-            ip.cursor = &ctr->cursor;
-            if ((e = cudaMemsetAsync(&ctr->cursor, 0, sizeof ctr->cursor, st))) return cuda_fail(p, e);
-            LAUNCH(SHUF_K_PLAN, launch_ip_stripes(ip, st));
-            LAUNCH(SHUF_K_HIST, launch_ip_classify(rp, ip, st, p->grid_ipc));
-            LAUNCH(SHUF_K_PLAN, launch_ip_plan(rp, ip, st));
-            LAUNCH(SHUF_K_SCATTER, launch_ip_permute(rp, ip, st, p->grid_ipp));
-            LAUNCH(SHUF_K_SCAN, launch_ip_fill(rp, ip, st, p->grid_ipp));
-            if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast_ip(rp, ip, st, p->grid_fast));
-            LAUNCH(SHUF_K_FINISH, launch_finish_ipchildren(rp, ip, st, p->grid_finish));
-            LAUNCH(SHUF_K_LEAF, launch_leaf_ipchildren(rp, ip, st, p->grid_leaf));
-            s0 = s1;
+    if (p->n <= p->S_fuse || max_levels == 0) {
+        if ((e = cudaMemsetAsync(ax, 0, l.segs[0], st))) return cuda_fail(p, e);  // header, counters, state
+        LAUNCH(SHUF_K_INIT, launch_ip_root(hdr, p->n, st));
+        if (p->n <= p->S_fuse) {
+            if (p->n <= p->L) LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, hdr->root_off, 1, st, 1));
+            else LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
         }
-        uint32_t nn = 0;
-        if ((e = cudaMemcpyAsync(&nn, &ctr->nnext[cur ^ 1u], 4, cudaMemcpyDeviceToHost, st))) return cuda_fail(p, e);
-        if ((e = cudaStreamSynchronize(st))) return cuda_fail(p, e);
-        if (nn > l.max_segs) return SHUF_ERR_DEPTH;
-        nseg = nn;
-        cur ^= 1u;
+        p->last_launches = launches;
+        return SHUF_OK;
     }
-    p->last_launches = launches;
+    if (!p->ip_exec || p->ip_ptr != ptr || p->ip_aux != aux || p->ip_maxlv != max_levels || p->ip_leaves != run_leaves) {
+        if (p->ip_exec) {
+            cudaGraphExecDestroy(p->ip_exec);
+            p->ip_exec = nullptr;
+        }
+        IpParams ip{};
+        ip.Z = l.Z;
+        ip.zseg = reinterpret_cast<uint32_t*>(ax + l.zseg);
+        ip.N = reinterpret_cast<uint64_t*>(ax + l.N);
+        ip.F = reinterpret_cast<uint32_t*>(ax + l.F);
+        ip.S = reinterpret_cast<uint64_t*>(ax + l.S);
+        ip.wr = reinterpret_cast<uint64_t*>(ax + l.wr);
+        ip.regpre = reinterpret_cast<uint32_t*>(ax + l.regpre);
+        ip.segtot = reinterpret_cast<uint64_t*>(ax + l.segtot);
+        ip.ovf = reinterpret_cast<uint32_t*>(ax + l.ovf);
+        ip.ovfd = ax + l.ovfd;
+        ip.pcnt = reinterpret_cast<uint32_t*>(ax + l.pcnt);
+        ip.part = ax + l.part;
+        ip.tags = reinterpret_cast<uint16_t*>(ax + l.tags);
+        ip.max_next = l.max_segs;
+        ip.cursor = &ctr->cursor;
+        ip.state = reinterpret_cast<IpState*>(ax + l.state);
+        ip.segbase[0] = reinterpret_cast<IpSeg*>(ax + l.segs[0]);
+        ip.segbase[1] = reinterpret_cast<IpSeg*>(ax + l.segs[1]);
+        ip.nnext_base = ctr->nnext;
+        if (!p->ip_cap_stream && (e = cudaStreamCreateWithFlags(&p->ip_cap_stream, cudaStreamNonBlocking)))
+            return cuda_fail(p, e);
+        cudaStream_t cs = p->ip_cap_stream;
+        IpState st0{};
+        st0.C = l.C;
+        st0.max_batches = (uint32_t)l.max_batches;
+        st0.batches = reinterpret_cast<IpBatch*>(ax + l.batches);
+        // Graph: memsets, init; WHILE(levels) { level_plan; WHILE(batches) { batch kernels; batch_next };
+        // level_next }.  Built by stream capture; the WHILE nodes are added mid-capture.
+        cudaGraph_t g = nullptr, bl = nullptr, bb = nullptr;
+        cudaGraphConditionalHandle hl = 0, hb = 0;
+        auto fail = [&](cudaError_t err) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(cs, &junk);
+            if (junk) cudaGraphDestroy(junk);
+            if (g) cudaGraphDestroy(g);
+            return cuda_fail(p, err);
+        };
+        auto add_while = [&](cudaGraphConditionalHandle h, cudaGraph_t* body) -> cudaError_t {
+            cudaStreamCaptureStatus cst;
+            cudaGraph_t cg = nullptr;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            cudaError_t err = cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &nd);
+            if (err) return err;
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            if ((err = cudaGraphAddNode(&node, cg, deps, nd, &cp))) return err;
+            *body = cp.conditional.phGraph_out[0];
+            return cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies);
+        };
+        uint64_t nodes = 0;
+        if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed))) return cuda_fail(p, e);
+        if ((e = cudaMemsetAsync(ax, 0, l.segs[0], cs))) return fail(e);  // header, counters, state, batches
+        if ((e = cudaMemsetAsync(ax + l.N, 0, l.S - l.N, cs))) return fail(e);          // N, F
+        if ((e = cudaMemsetAsync(ax + l.ovf, 0, l.ovfd - l.ovf, cs))) return fail(e);
+        if ((e = launch_ip_init(ip, hdr, p->n, st0, cs))) return fail(e);  // (kernel argument: no host memory in the graph)
+        {
+            cudaStreamCaptureStatus cst;
+            if ((e = cudaStreamGetCaptureInfo(cs, &cst, nullptr, &g))) return fail(e);
+            if ((e = cudaGraphConditionalHandleCreate(&hl, g, 1, cudaGraphCondAssignDefault))) return fail(e);
+        }
+        if ((e = add_while(hl, &bl))) return fail(e);
+        if ((e = cudaStreamEndCapture(cs, &g))) return fail(e);
+        // level body
+        if ((e = cudaGraphConditionalHandleCreate(&hb, bl, 0, cudaGraphCondAssignDefault))) return fail(e);
+        if ((e = cudaStreamBeginCaptureToGraph(cs, bl, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+            return fail(e);
+        if ((e = launch_ip_level_plan(rp, ip, hb, cs))) return fail(e);
+        if ((e = add_while(hb, &bb))) return fail(e);
+        if ((e = launch_ip_level_next(rp, ip, hl, cs))) return fail(e);
+        {
+            cudaGraph_t out = nullptr;
+            if ((e = cudaStreamEndCapture(cs, &out))) return fail(e);
+        }
+        // batch body
+        if ((e = cudaStreamBeginCaptureToGraph(cs, bb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)))
+            return fail(e);
+        if ((e = launch_ip_stripes(ip, cs))) return fail(e);
+        if ((e = launch_ip_classify(rp, ip, cs, p->grid_ipc))) return fail(e);
+        if ((e = launch_ip_plan(rp, ip, cs))) return fail(e);
+        if ((e = launch_ip_permute(rp, ip, cs, p->grid_ipp))) return fail(e);
+        if ((e = launch_ip_fill(rp, ip, cs, p->grid_ipp))) return fail(e);
+        nodes = 6;
+        if (p->fast) {
+            if ((e = launch_finish_fast_ip(rp, ip, cs, p->grid_fast))) return fail(e);
+            ++nodes;
+        }
+        if ((e = launch_finish_ipchildren(rp, ip, cs, p->grid_finish))) return fail(e);
+        if ((e = launch_leaf_ipchildren(rp, ip, cs, p->grid_leaf))) return fail(e);
+        if ((e = launch_ip_batch_next(ip, hb, cs))) return fail(e);
+        {
+            cudaGraph_t out = nullptr;
+            if ((e = cudaStreamEndCapture(cs, &out))) return fail(e);
+        }
+        e = cudaGraphInstantiate(&p->ip_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e) {
+            p->ip_exec = nullptr;
+            return cuda_fail(p, e);
+        }
+        p->ip_ptr = ptr;
+        p->ip_aux = aux;
+        p->ip_maxlv = max_levels;
+        p->ip_leaves = run_leaves;
+        p->ip_nodes = nodes + 2;  // + init, plan, next per level / batch (counted by the caller as launches)
+    }
+    if ((e = cudaGraphLaunch(p->ip_exec, st))) return cuda_fail(p, e);
+    p->last_launches = p->ip_nodes;
     return SHUF_OK;
 }
 
@@ -880,6 +948,8 @@ extern "C" void shuf_destroy(shuf_plan_t p) {
         cudaEventDestroy(p->ev_fork);
         cudaEventDestroy(p->ev_join);
     }
+    if (p && p->ip_exec) cudaGraphExecDestroy(p->ip_exec);
+    if (p && p->ip_cap_stream) cudaStreamDestroy(p->ip_cap_stream);
     delete p;
 }
 

@@ -19,7 +19,7 @@ constexpr uint32_t kMaxLevels = 256;
 constexpr uint32_t kScatterTileBytes = 32768; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
 constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
 constexpr uint32_t kIpBlockBytes = 128;     // in-place mode block (kernels_inplace.cu)
-constexpr uint32_t kIpBatchCap = 1024;      // in-place mode: stripes (and segments) per batch
+constexpr uint32_t kIpBatchCap = 2048;      // in-place mode: stripes (and segments) per batch
 
 // ---------------------------------------------------------- descriptors ---
 // A segment processed by an HBM-resident ("global") scatter level.
@@ -151,12 +151,31 @@ struct IpCounters {
     unsigned long long cursor;  // k_ip_permute pair cursor
 };
 
-// One batch of segments of one in-place level.
+// One batch of an in-place level: segments [s0, s0+nseg) of the level's
+// list, nz stripes.
+struct IpBatch {
+    uint32_t s0, nseg, nz, first;  // first: scratch of k_ip_level_plan
+};
+
+// Device-resident loop state of the in-place mode.  The whole level loop runs
+// on the device (a CUDA graph with two nested conditional WHILE nodes, levels
+// and batches; shuf_api.cu): every batch kernel resolves its batch from here.
+struct IpState {
+    uint32_t level, cur, batch, nbatch;  // cur: parity of the level's segment list
+    uint32_t nseg;                       // segments of the current level
+    uint32_t C;                          // stripe window per batch (batches hold < 2C stripes)
+    uint32_t max_batches, pad;
+    IpBatch* batches;
+};
+
+// One batch of segments of one in-place level.  With `state` set, the
+// fields marked (*) are resolved on the device from the loop state at the
+// start of every kernel (ip_resolve); the host fills the rest.
 struct IpParams {
-    IpSeg* segs;              // the batch's segments
-    uint32_t nseg;            // segments in the batch
-    uint32_t nstripes;        // stripes in the batch
-    uint32_t level;
+    IpSeg* segs;              // (*) the batch's segments
+    uint32_t nseg;            // (*) segments in the batch
+    uint32_t nstripes;        // (*) stripes in the batch
+    uint32_t level;           // (*)
     uint32_t pad;
     uint64_t Z;               // stripe length (elements, multiple of the block)
     uint32_t* zseg;           // stripe -> batch segment
@@ -171,11 +190,30 @@ struct IpParams {
     uint32_t* pcnt;           // [nstripes*k] partial counts
     unsigned char* part;      // [nstripes*k] partial buffers (one block each)
     uint16_t* tags;           // per block slot: bucket / empty / read
-    IpSeg* next;              // next level's list
-    uint32_t* nnext;
+    IpSeg* next;              // (*) next level's list
+    uint32_t* nnext;          // (*)
     uint64_t max_next;
     unsigned long long* cursor;
+    IpState* state;           // device loop state
+    IpSeg* segbase[2];        // the two level lists (by parity)
+    uint32_t* nnext_base;     // their lengths (IpCounters::nnext)
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ IpParams ip_resolve(IpParams ip) {
+    if (!ip.state) return ip;
+    const IpState* st = ip.state;
+    const uint32_t cur = st->cur;
+    const IpBatch bt = st->batches[st->batch];
+    ip.segs = ip.segbase[cur] + bt.s0;
+    ip.nseg = bt.nseg;
+    ip.nstripes = bt.nz;
+    ip.level = st->level;
+    ip.next = ip.segbase[cur ^ 1u];
+    ip.nnext = ip.nnext_base + (cur ^ 1u);
+    return ip;
+}
+#endif
 
 // ------------------------------------------------------ host launchers ---
 cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid);
@@ -204,6 +242,11 @@ cudaError_t configure_leaf(uint32_t eb, uint32_t L);
 cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks);
 uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L);
 cudaError_t launch_ip_root(Header* hdr, uint64_t n, cudaStream_t s);
+cudaError_t launch_ip_init(const IpParams& ip, Header* hdr, uint64_t n, const IpState& init, cudaStream_t s);
+cudaError_t launch_ip_level_plan(const RunParams& rp, const IpParams& ip, cudaGraphConditionalHandle hb, cudaStream_t s);
+cudaError_t launch_ip_batch_next(const IpParams& ip, cudaGraphConditionalHandle hb, cudaStream_t s);
+cudaError_t launch_ip_level_next(const RunParams& rp, const IpParams& ip, cudaGraphConditionalHandle hl,
+                                 cudaStream_t s);
 cudaError_t launch_ip_stripes(const IpParams& ip, cudaStream_t s);
 cudaError_t launch_ip_classify(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);
 cudaError_t launch_ip_plan(const RunParams& rp, const IpParams& ip, cudaStream_t s);

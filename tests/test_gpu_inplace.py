@@ -51,7 +51,7 @@ SHAPES = [
     # n, k, L, seed -- all reach at least one in-place HBM level
     (100_003, 256, 4096, 5), (1 << 20, 256, 4096, 1), (777_777, 7, 300, 6), (300_001, 1000, 50, 7),
     (200_000, 2, 1, 8), (3_000_000, 256, 4096, 11), (2_000_000, 64, 40, 3), (65_537, 1024, 16, 2),
-    (24_000_000, 1024, 4096, 12),  # level 1: 1024 segments > S_fuse = one full batch (kIpBatchCap)
+    (24_000_000, 1024, 4096, 12),  # level 1: 1024 segments > S_fuse in one level (batches of < 2C stripes)
 ]
 
 
