@@ -104,7 +104,8 @@ shuf_status shuf_segmented(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, 
 /* In-place mode (the paper's in-place motivation P:32-36,
  * P:39-43).  Shuffles ptr[0..n) using an auxiliary DEVICE buffer `aux` of
  * shuf_aux_bytes_inplace() bytes, about 2 bytes per 128-byte block of ptr plus
- * O(k * 1024 * 128 B) for bucket buffers -- a few percent of n*elem_bytes
+ * O(k * 2048 * 128 B) for bucket buffers -- under 5 % of n*elem_bytes above
+ * 1 GiB
  * instead of shuf_run's n*elem_bytes ping-pong buffer.  Each level longer than
  * the fused size classifies elements into 128-byte blocks in place, permutes
  * the blocks into their buckets' regions and fills the bucket heads and tails
@@ -114,9 +115,12 @@ shuf_status shuf_segmented(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, 
  * on atomics: the result is a uniformly random permutation but NOT
  * reproducible and NOT equal to shuf_run's.  Segments of at most the fused
  * size and leaves run the same (deterministic) in-place finish and leaf
- * kernels as shuf_run.  Host-synchronous: the call synchronises `stream` once
- * per level (it reads back the next level's segment list to batch it).
- * ptr and aux must be 16-byte aligned; aux is overwritten; no allocation. */
+ * kernels as shuf_run.  Stream-ordered, no host synchronisation: the level
+ * loop runs on the device as one launch of a CUDA graph with conditional
+ * WHILE nodes (levels, batches of segments) that the plan builds on the first
+ * call for a given (ptr, aux) and caches; calls with other buffers rebuild it.
+ * ptr and aux must be 16-byte aligned; aux is overwritten; no allocation of
+ * device memory (the graph itself is host-side driver state). */
 shuf_status shuf_aux_bytes_inplace(shuf_plan_t p, uint64_t *bytes);
 shuf_status shuf_run_inplace(shuf_plan_t p, void *ptr, void *aux, uint64_t aux_bytes, void *stream);
 
