@@ -97,6 +97,41 @@ def workload_bytes(w, stats):
     return 2 * w.elem_bytes * (scattered + w.n), scattered
 
 
+def gpu_baselines(x, n: int, ms_ours: float, dev, reps: int = 3) -> dict:
+    """Library GPU shuffles of the same resident input, timed the same way
+    (CUDA events, after one warm-up): x[randperm(n)] (PyTorch) and the paper's
+    SortShuffle (attach a random key, sort by it) as a CUB radix
+    sort of random 64-bit keys.  Uniform shuffles, not D6's permutation:
+    comparison points only, never the product path."""
+    import torch
+
+    def randperm_gather():
+        return x.index_select(0, torch.randperm(n, device=dev))
+
+    def sort_shuffle():
+        keys = torch.randint(-(1 << 63), (1 << 63) - 1, (n,), dtype=torch.int64, device=dev)
+        return x.index_select(0, torch.sort(keys).indices)
+
+    out = {}
+    for name, fn in (("torch_randperm_gather", randperm_gather), ("sort_shuffle_u64_keys", sort_shuffle)):
+        try:
+            fn()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / reps
+            out[name] = {"ms": round(ms, 3), "value": n / (ms / 1e3), "unit": "elements/s",
+                         "ours_speedup": round(ms / ms_ours, 2)}
+        except RuntimeError as ex:  # out of memory on huge workloads
+            out[name] = {"unavailable": str(ex).splitlines()[0][:120]}
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---- multi-rank host logic (replicas only, DESIGN.md 8); tested with gloo on CPU
 def rank_seed(seed: int, rank: int) -> int:
     """Every rank shuffles its own independent problem."""
@@ -190,6 +225,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 25)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-gpu-baselines", action="store_true",
+                    help="skip the library GPU shuffles timed beside ours (SURVEY 8(f) NEXT-4)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -357,6 +394,9 @@ def main():
         del host_in, host_out, xbuf
 
     cpu = None
+    gbase = None
+    if rank == 0 and world == 1 and not args.no_gpu_baselines and d_off is None:
+        gbase = gpu_baselines(x, w.n, ms, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w if w.kind != "segmented" else synth.WORKLOADS["c1"], min(args.cpu_sample, w.n))
 
@@ -377,7 +417,7 @@ def main():
             "frac_of_measured_copy": eff_gbps / hbm_peak, "effective_bytes_per_step": eff_bytes,
             "elements_scattered_per_step": scattered, "levels": {"hbm": stats["scattered_hbm"],
                                                                  "smem": stats["scattered_smem"]},
-            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "gpu_baselines": gbase, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "device": device_facts(dev),
         }
         print(json.dumps(line), flush=True)

@@ -88,7 +88,14 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
         top -= (int32_t)c;
     }
 }
-uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L) { return kLeafWarps * (leaf_slot_bytes(eb, L) + 16); }
+// Warps per leaf CTA: 4, or fewer when 4 slots exceed the shared memory
+// (e.g. 16-byte elements with L = 4096: a 64 KiB slot per warp).
+uint32_t leaf_warps(uint32_t eb, uint32_t L) {
+    uint32_t w = kLeafWarps;
+    while (w > 1 && w * (leaf_slot_bytes(eb, L) + 16) > kSmemLimit) --w;
+    return w;
+}
+uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L) { return leaf_warps(eb, L) * (leaf_slot_bytes(eb, L) + 16); }
 
 struct Leaf {
     uint64_t start, len, origin, key;
@@ -209,7 +216,8 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
     const uint64_t units = ls.units();
     const bool copy_out = src != rp.buf0;
     unsigned long long fyn = 0, fin = 0;
-    for (uint64_t u = (uint64_t)blockIdx.x * kLeafWarps + warp; u < units; u += (uint64_t)gridDim.x * kLeafWarps) {
+    const uint32_t nw = blockDim.x >> 5;  // leaf_warps()
+    for (uint64_t u = (uint64_t)blockIdx.x * nw + warp; u < units; u += (uint64_t)gridDim.x * nw) {
         const Leaf lf = ls.get(u, lane);
         const uint64_t start = lf.start, len = lf.len, origin = lf.origin, key = lf.key;
         const bool fy = len >= 2 && len <= rp.L && rp.run_leaves;
@@ -369,13 +377,13 @@ cudaError_t configure_leaf(uint32_t eb, uint32_t L) {
 }
 
 cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, leaf_fn(eb, 0), kLeafThreads,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, leaf_fn(eb, 0), 32 * leaf_warps(eb, L),
                                                          leaf_smem_bytes(eb, L));
 }
 
 cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp, (void*)&lp};
-    return cudaLaunchKernel(leaf_fn(rp.eb, 0), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L),
+    return cudaLaunchKernel(leaf_fn(rp.eb, 0), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L),
                             s);
 }
 
@@ -383,18 +391,18 @@ cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets,
                                  cudaStream_t s, int grid) {
     uint32_t U = leaf_unit(rp.eb, rp.L, num_segments ? rp.n / num_segments : 0);
     void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments, (void*)&U};
-    return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L),
+    return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L),
                             s);
 }
 
 cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp};
-    return cudaLaunchKernel(leaf_fn(rp.eb, 2), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L), s);
+    return cudaLaunchKernel(leaf_fn(rp.eb, 2), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L), s);
 }
 
 cudaError_t launch_leaf_ipchildren(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp, (void*)&ip};
-    return cudaLaunchKernel(leaf_fn(rp.eb, 3), dim3(grid), dim3(kLeafThreads), args, leaf_smem_bytes(rp.eb, rp.L), s);
+    return cudaLaunchKernel(leaf_fn(rp.eb, 3), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L), s);
 }
 
 }  // namespace shuf

@@ -52,6 +52,9 @@ struct shuf_plan_s {
     uint32_t ip_maxlv;
     int ip_leaves;
     uint64_t ip_nodes;
+    // elem_bytes outside {4, 8, 16}: the gather route (kernels_gather.cu) --
+    // `idx` shuffles the index array 0..n-1, then the elements move once
+    struct shuf_plan_s* idx;
     int rank_ordered;
     uint32_t finish_smem, scatter_smem;
     int last_cuda_error;
@@ -247,9 +250,30 @@ static void compute_ip_layout(shuf_plan_s* p) {
 
 extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, uint32_t L, uint64_t seed) {
     g_last_status = SHUF_OK;
-    if (!(elem_bytes == 4 || elem_bytes == 8 || elem_bytes == 16) && elem_bytes != 0) {
+    if (elem_bytes > kMaxGatherElem) {
         g_last_status = SHUF_ERR_UNSUPPORTED;
         return nullptr;
+    }
+    if (elem_bytes != 0 && !(elem_bytes == 4 || elem_bytes == 8 || elem_bytes == 16)) {
+        // gather route: D6's permutation of n elements does not depend on their size
+        shuf_plan_s* ix = shuf_plan(n, n <= 0xFFFFFFFFull ? 4u : 8u, k, L, seed);
+        if (!ix) return nullptr;
+        shuf_plan_s* p = new (std::nothrow) shuf_plan_s();
+        if (!p) {
+            shuf_destroy(ix);
+            g_last_status = SHUF_ERR_INVALID_ARG;
+            return nullptr;
+        }
+        p->n = n;
+        p->eb = elem_bytes;
+        p->k = k;
+        p->L = L;
+        p->seed = seed;
+        p->S_fuse = ix->S_fuse;
+        p->chunk = ix->chunk;
+        p->levels = ix->levels;
+        p->idx = ix;
+        return p;
     }
     if (elem_bytes == 0 || k < 2 || k > 65536 || L < 1) {
         g_last_status = SHUF_ERR_INVALID_ARG;
@@ -315,9 +339,14 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
 
 extern "C" shuf_status shuf_last_status(void) { return g_last_status; }
 
+// Gather route scratch: [index plan's scratch | index array | staging buffer].
+static uint64_t gather_extra(const shuf_plan_s* p) {
+    return align_up(p->n * p->idx->eb, 256) + align_up(p->n * p->eb, 256);
+}
+
 extern "C" shuf_status shuf_scratch_bytes(shuf_plan_t p, uint64_t* bytes) {
     if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
-    *bytes = p->lay.total;
+    *bytes = p->idx ? align_up(p->idx->lay.total, 256) + gather_extra(p) : p->lay.total;
     return SHUF_OK;
 }
 
@@ -481,9 +510,14 @@ static uint64_t seg0_bound(const shuf_plan_s* p, uint64_t num_segments) {
 
 extern "C" shuf_status shuf_scratch_bytes_segmented(shuf_plan_t p, uint64_t num_segments, uint64_t* bytes) {
     if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) {
+        *bytes = align_up(compute_layout(p->idx, seg0_bound(p->idx, num_segments), true).total, 256) + gather_extra(p);
+        return SHUF_OK;
+    }
     *bytes = compute_layout(p, seg0_bound(p, num_segments), true).total;
     return SHUF_OK;
 }
+
 
 // Optional per-launch CUDA-event bracketing (shuf_profile_run only).
 struct Prof {
@@ -601,19 +635,50 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     return SHUF_OK;
 }
 
+// The gather route: iota -> the index plan's shuffle (single, segmented or
+// level-limited) -> out[i] = in[idx[i]] into the staging buffer -> copy back.
+static shuf_status gather_route(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets, uint64_t nsegs, void* scratch,
+                                uint64_t scratch_bytes, cudaStream_t st, uint32_t max_levels, int run_leaves,
+                                Prof* prof) {
+    shuf_plan_s* ix = p->idx;
+    const uint64_t sub = align_up(d_offsets ? compute_layout(ix, seg0_bound(ix, nsegs), true).total : ix->lay.total, 256);
+    if (scratch_bytes < sub + gather_extra(p)) return SHUF_ERR_SCRATCH;
+    unsigned char* sc = static_cast<unsigned char*>(scratch);
+    unsigned char* idxa = sc + sub;
+    unsigned char* stage = idxa + align_up(p->n * ix->eb, 256);
+    cudaError_t e = device_setup(ix);
+    if (e) return cuda_fail(p, e);
+    const int grid = ix->sms * 8;
+    if ((e = launch_iota(idxa, ix->eb, p->n, st, grid))) return cuda_fail(p, e);
+    shuf_status r = enqueue(ix, idxa, d_offsets, nsegs, sc, st, max_levels, run_leaves, prof);
+    if (r) {
+        p->last_cuda_error = ix->last_cuda_error;
+        return r;
+    }
+    if ((e = launch_gather(ptr, stage, idxa, ix->eb, p->n, p->eb, st, grid))) return cuda_fail(p, e);
+    if ((e = cudaMemcpyAsync(ptr, stage, p->n * p->eb, cudaMemcpyDeviceToDevice, st))) return cuda_fail(p, e);
+    p->last_hdr = ix->last_hdr;
+    p->last_launches = ix->last_launches + 2;
+    return SHUF_OK;
+}
+
 extern "C" shuf_status shuf_run(shuf_plan_t p, void* ptr, void* scratch, uint64_t scratch_bytes, void* stream) {
-    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes, p && p->idx ? 0 : ~0ull);
     if (s) return s;
     if (p->n <= 1) {
         p->last_launches = 0;
         return SHUF_OK;
     }
+    if (p->idx)
+        return gather_route(p, ptr, nullptr, 0, scratch, scratch_bytes, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu,
+                            1, nullptr);
     return enqueue(p, ptr, nullptr, 0, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
 }
 
 // ------------------------------------------------------------ in-place ---
 extern "C" shuf_status shuf_aux_bytes_inplace(shuf_plan_t p, uint64_t* bytes) {
     if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) return SHUF_ERR_UNSUPPORTED;  // the in-place mode moves 4/8/16-byte elements only
     *bytes = p->ipl.total;
     return SHUF_OK;
 }
@@ -806,6 +871,7 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
 
 static shuf_status check_inplace_args(shuf_plan_s* p, void* ptr, void* aux, uint64_t aux_bytes) {
     if (!p) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) return SHUF_ERR_UNSUPPORTED;
     if (p->n > 1 && (!ptr || !aux)) return SHUF_ERR_INVALID_ARG;
     if (((uintptr_t)ptr & 15u) || ((uintptr_t)aux & 15u)) return SHUF_ERR_ALIGNMENT;
     if (p->n > 1 && aux_bytes < p->ipl.total) return SHUF_ERR_SCRATCH;
@@ -829,16 +895,19 @@ extern "C" shuf_status shuf_debug_inplace_levels(shuf_plan_t p, void* ptr, void*
 
 extern "C" shuf_status shuf_debug_run_levels(shuf_plan_t p, void* ptr, void* scratch, uint64_t scratch_bytes,
                                              void* stream, uint32_t max_levels, int run_leaves) {
-    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes);
+    shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes, p && p->idx ? 0 : ~0ull);
     if (s) return s;
     if (p->n <= 1) return SHUF_OK;
+    if (p->idx)
+        return gather_route(p, ptr, nullptr, 0, scratch, scratch_bytes, static_cast<cudaStream_t>(stream), max_levels,
+                            run_leaves ? 1 : 0, nullptr);
     return enqueue(p, ptr, nullptr, 0, scratch, static_cast<cudaStream_t>(stream), max_levels, run_leaves ? 1 : 0);
 }
 
 extern "C" shuf_status shuf_segmented(shuf_plan_t p, void* ptr, const uint64_t* d_offsets, uint64_t num_segments,
                                       void* scratch, uint64_t scratch_bytes, void* stream) {
     shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes,
-                                   p ? compute_layout(p, seg0_bound(p, num_segments), true).total : 0);
+                                   p && !p->idx ? compute_layout(p, seg0_bound(p, num_segments), true).total : 0);
     if (s) return s;
     if (!d_offsets) return SHUF_ERR_INVALID_ARG;
     if ((uintptr_t)d_offsets & 7u) return SHUF_ERR_ALIGNMENT;
@@ -846,6 +915,9 @@ extern "C" shuf_status shuf_segmented(shuf_plan_t p, void* ptr, const uint64_t* 
         p->last_launches = 0;
         return SHUF_OK;
     }
+    if (p->idx)
+        return gather_route(p, ptr, d_offsets, num_segments, scratch, scratch_bytes, static_cast<cudaStream_t>(stream),
+                            0xFFFFFFFFu, 1, nullptr);
     return enqueue(p, ptr, d_offsets, num_segments, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
 }
 
@@ -853,7 +925,9 @@ extern "C" shuf_status shuf_profile_run(shuf_plan_t p, void* ptr, const uint64_t
                                         void* scratch, uint64_t scratch_bytes, void* stream, float* ms_by_class,
                                         uint32_t* launches_by_class) {
     shuf_status s = check_run_args(p, ptr, scratch, scratch_bytes,
-                                   p && d_offsets ? compute_layout(p, seg0_bound(p, num_segments), true).total : ~0ull);
+                                   p && p->idx ? 0
+                                   : p && d_offsets ? compute_layout(p, seg0_bound(p, num_segments), true).total
+                                                    : ~0ull);
     if (s) return s;
     if (!ms_by_class || !launches_by_class) return SHUF_ERR_INVALID_ARG;
     for (int c = 0; c < SHUF_K_CLASSES; ++c) {
@@ -864,7 +938,8 @@ extern "C" shuf_status shuf_profile_run(shuf_plan_t p, void* ptr, const uint64_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Prof prof;
     prof.st = st;
-    s = enqueue(p, ptr, d_offsets, num_segments, scratch, st, 0xFFFFFFFFu, 1, &prof);
+    s = p->idx ? gather_route(p, ptr, d_offsets, num_segments, scratch, scratch_bytes, st, 0xFFFFFFFFu, 1, &prof)
+               : enqueue(p, ptr, d_offsets, num_segments, scratch, st, 0xFFFFFFFFu, 1, &prof);
     if (s) return s;
     cudaError_t e = cudaStreamSynchronize(st);
     if (e) return cuda_fail(p, e);
@@ -949,6 +1024,7 @@ extern "C" void shuf_destroy(shuf_plan_t p) {
         cudaEventDestroy(p->ev_join);
     }
     if (p && p->ip_exec) cudaGraphExecDestroy(p->ip_exec);
+    if (p && p->idx) shuf_destroy(p->idx);
     if (p && p->ip_cap_stream) cudaStreamDestroy(p->ip_cap_stream);
     delete p;
 }

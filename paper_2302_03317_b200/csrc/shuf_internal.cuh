@@ -12,6 +12,7 @@ namespace shuf {
 constexpr int kWarps = 16;                 // warps per CTA in the ranking kernels
 constexpr int kThreads = kWarps * 32;      // 512
 constexpr uint32_t kMaxK = 1024;           // device bucket-count limit
+constexpr uint32_t kMaxGatherElem = 256;   // largest element (bytes); sizes other than 4/8/16 take the gather route
 constexpr uint32_t kScanTile = 4096;       // entries per decoupled-lookback tile
 constexpr uint32_t kSmemLimit = 227 * 1024;
 constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
@@ -257,6 +258,9 @@ cudaError_t launch_leaf_ipchildren(const RunParams& rp, const IpParams& ip, cuda
 cudaError_t configure_inplace(uint32_t eb, uint32_t k);
 cudaError_t occupancy_inplace(uint32_t eb, uint32_t k, int* classify, int* permute);
 uint32_t ip_classify_smem_bytes(uint32_t eb, uint32_t k);
+cudaError_t launch_iota(void* idx, uint32_t ieb, uint64_t n, cudaStream_t s, int grid);
+cudaError_t launch_gather(const void* in, void* out, const void* idx, uint32_t ieb, uint64_t n, uint32_t eb,
+                          cudaStream_t s, int grid);
 cudaError_t launch_copy_big(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_rank_order_probe(int grid, uint32_t* d_violations, cudaStream_t s);
 uint32_t scatter_smem_bytes(uint32_t eb, uint32_t k);

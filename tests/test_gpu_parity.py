@@ -55,6 +55,7 @@ CASES = [
     (300_001, 1000, 50, 7, 4),                                          # k with rejections
     (200_000, 2, 1, 8, 4),                                              # deepest recursion
     (123_457, 64, 2048, 9, 8), (99_991, 1024, 2048, 10, 16),            # element sizes
+    (2_500_000, 256, 4096, 12, 16),                                     # 16-byte leaves of ~L: 2-warp leaf CTAs
     (3_000_000, 256, 4096, 11, 4),                                      # 1 HBM level (+1 planned spare), fused
     (1 << 25, 64, 300, 21, 4),                                          # HOT's shape: 2 HBM levels, then the
     (1 << 26, 256, 64, 22, 4),                                          #  pipelined finish, then FY leaves

@@ -39,7 +39,7 @@ def test_sm100a_code_in_library():
 
 
 @pytest.mark.parametrize("args,code", [
-    ((100, 3, 256, 16, 1), 2),      # elem_bytes outside {4, 8, 16}: unsupported on device
+    ((100, 257, 256, 16, 1), 2),    # elem_bytes above 256: unsupported on device
     ((100, 0, 256, 16, 1), 1),      # elem_bytes 0: invalid
     ((100, 4, 1, 16, 1), 1),        # k < 2
     ((100, 4, 70000, 16, 1), 1),    # k > 2^16
@@ -63,6 +63,22 @@ def test_plan_scratch_and_levels(L):
     big = shuf.shuf_plan(1 << 32, 16, 1024, 2048, 11)
     assert big.planned_levels >= 2
     assert big.scratch_bytes >= (1 << 32) * 16
+
+
+@pytest.mark.parametrize("eb", [1, 2, 3, 12, 32, 64, 256])
+def test_gather_route_plans(L, eb):
+    """Sizes outside {4, 8, 16} plan the gather route (NEXT-4): the index plan's
+    scratch (u32 indices below 2^32 elements) + index array + staging rows."""
+    n = 1 << 24
+    p = shuf.shuf_plan(n, eb, 256, 4096, 1)
+    ix = shuf.shuf_plan(n, 4, 256, 4096, 1)
+    assert p.planned_levels == ix.planned_levels
+    assert p.scratch_bytes >= ix.scratch_bytes + n * 4 + n * eb
+    assert p.scratch_bytes < ix.scratch_bytes + n * 4 + n * eb + 4096
+    big = shuf.shuf_plan((1 << 32) + 5, eb, 256, 4096, 1)  # u64 indices
+    assert big.scratch_bytes >= ((1 << 32) + 5) * (8 + eb)
+    code = L.shuf_aux_bytes_inplace(p.handle, ctypes.byref(ctypes.c_uint64()))
+    assert code == 2  # the in-place mode moves 4/8/16-byte elements only
 
 
 @pytest.mark.parametrize("n,eb,k,L_,bound", [
