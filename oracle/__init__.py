@@ -88,6 +88,12 @@ def lib():
         L.oracle_points.restype = i32
         L.oracle_sim_rough_scatter.argtypes = [u64, u32, u64, u32, vp, vp]
         L.oracle_sim_rough_scatter.restype = i32
+        L.oracle_ipsc_draw.argtypes = [u64, u32, u32, u32, u32, u64, u32]
+        L.oracle_ipsc_draw.restype = u32
+        L.oracle_ipsc_depth.argtypes = [u64, u32]
+        L.oracle_ipsc_depth.restype = u32
+        L.oracle_ipsc_shuffle.argtypes = [vp, u64, u32, u32, u32, u64, u32, i32, vp, vp]
+        L.oracle_ipsc_shuffle.restype = i32
         _lib = L
     return _lib
 
@@ -215,3 +221,40 @@ def sim_rough_scatter(n: int, k: int, seed: int, runs: int):
     if rc:
         raise RuntimeError(f"oracle_sim_rough_scatter failed with status {rc}")
     return T, M
+
+
+class IpscStats(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint64) for f in
+                ("segments", "rough_steps", "merge_swaps", "staged", "transfers", "dsum", "leaves")]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+IPSC_RS, IPSC_FM, IPSC_FY = 7, 8, 9
+
+
+def ipsc_draw(K: int, tag: int, c0: int, c1: int, level: int, a: int, bound: int) -> int:
+    """D10 draw: first Lemire32-accepted word of Philox(K, (c0, c1, lo32 a,
+    tag | level << 8 | (hi32 a & 0xFFFF) << 16)) for the bound."""
+    return int(lib().oracle_ipsc_draw(K, tag, c0, c1, level, a, bound))
+
+
+def ipsc_depth(m: int, k: int) -> int:
+    """D10: ParRoughScatter tree depth t = min(11, floor(log2(m / k^2)))."""
+    return int(lib().oracle_ipsc_depth(m, k))
+
+
+def ipsc_shuffle(data: np.ndarray, k: int, L: int, seed: int, max_levels: int = ALL_LEVELS,
+                 run_leaves: bool = True, stats: bool = False):
+    """D10 (NEXT-2): the paper's In-Place ScatterShuffle (P:150-265, P:322-425,
+    P:479-491) with deterministic counter-based draws.  Returns the shuffled
+    copy, and with stats=True also (stats dict, level-0 final bucket sizes)."""
+    a = np.ascontiguousarray(data).copy()
+    st = IpscStats()
+    sizes0 = np.zeros(k, dtype=np.uint64)
+    rc = lib().oracle_ipsc_shuffle(_ptr(a), a.shape[0], _elem_bytes(a), k, L, seed, max_levels,
+                                   1 if run_leaves else 0, ctypes.byref(st), _ptr(sizes0))
+    if rc:
+        raise RuntimeError(f"oracle_ipsc_shuffle failed with status {rc}")
+    return (a, st.as_dict(), sizes0) if stats else a

@@ -665,3 +665,262 @@ int oracle_sim_rough_scatter(uint64_t n, uint32_t k, uint64_t seed, uint32_t run
     free(s);
     return 0;
 }
+
+/* ------------------------------------------- D10 (NEXT-2) -- */
+/* The paper's own In-Place ScatterShuffle, made deterministic with
+ * counter-based draws (D10).  Per segment [a, a+m) at level l with
+ * m > L (Fig. 2):
+ *   buckets   k contiguous buckets of capacities c_i = floor((i+1)m/k) -
+ *             floor(im/k) ("equal sizes n/k up to rounding"), each a
+ *             triple (b_i, s_i, e_i): [b, s) placed, [s, e) staged;
+ *   ParRough the buckets are split in halves recursively to
+ *             depth t = min(11, floor(log2(m / k^2))) (base case N0 = k^2,
+ *             P:506; at most 2^11 subtasks); heap-numbered nodes, root
+ *             1, children 2v, 2v+1 taking [lo, lo + floor((hi-lo)/2)) and the
+ *             rest of every bucket range of v.  Post-order: a leaf starts
+ *             all-staged; an inner node first merges its children bucket by
+ *             bucket ("swapping the staged items of the first half to the
+ *             second half"): with A = e - s staged in the first half
+ *             and B = s' - b' placed in the second, swap X[s + x] <-> X[s' - 1
+ *             - x] for x < min(A, B) -> (b, s + B, e').  Then, unless a bucket
+ *             is full, RoughScatter: repeat { j = draw(RS, step, v)
+ *             in [0, k); swap X[s_0] <-> X[s_j] (skipped if j = 0); s_j++;
+ *             stop if s_j = e_j }.
+ *   Fine at the root: n_i = s_i - b_i placed, R = sum of
+ *             the staged; N' = counts of R uniform draws draw(FM, r) (a
+ *             multinomial(R, 1/k) variate); n^f_i = n_i + N'_i;
+ *             TwoSweep with D_i = sum_{j<=i} (n^f_j - c_j):
+ *             ascending i = 0..k-2, -D_i > 0 times B_i's last (staged) slot
+ *             moves to B_{i+1} (e_i--, b_{i+1}--, then X[b_{i+1}] <->
+ *             X[s_{i+1} - 1] if B_{i+1} has placed items, s_{i+1}--);
+ *             descending i = k-2..0, D_i > 0 times B_{i+1}'s first slot moves
+ *             to B_i (X[b_{i+1}] <-> X[s_{i+1}] if B_{i+1} has placed items,
+ *             b_{i+1}++, s_{i+1}++, e_i++).  Stash: with p_0 < .. < p_{R-1}
+ *             the staged positions, swap X[a+t] <-> X[p_t] for t = 0..R-1,
+ *             Fisher-Yates X[a .. a+R) with partners draw(FY, i) in [0, i],
+ *             undo the swaps for t = R-1..0.
+ *   recurse   on the k final buckets at level l+1; a segment of at
+ *             most L elements is a Fisher-Yates leaf (D5, as D6).
+ * draw(tag, c0, c1): words w0..w3 of Philox(K, (c0, c1, lo32 a, tag | l << 8 |
+ * (hi32 a & 0xFFFF) << 16)); the first word Lemire32 accepts for the bound, or
+ * (w0 * bound) >> 32 if all four reject (probability < 2^-64).  Tags RS = 7,
+ * FM = 8, FY = 9 (D3 holds 1..6).                                  */
+#define IPSC_RS 7u
+#define IPSC_FM 8u
+#define IPSC_FY 9u
+#define IPSC_TMAX 11u
+
+uint32_t oracle_ipsc_draw(uint64_t K, uint32_t tag, uint32_t c0, uint32_t c1, uint32_t level, uint64_t a,
+                          uint32_t bound)
+{
+    uint32_t key[2], ctr[4], w[4], out = 0;
+    key_words(K, key);
+    ctr[0] = c0;
+    ctr[1] = c1;
+    ctr[2] = (uint32_t)a;
+    ctr[3] = tag | (level << 8) | (((uint32_t)(a >> 32) & 0xFFFFu) << 16);
+    oracle_philox4x32_10(ctr, key, w);
+    for (int q = 0; q < 4; ++q)
+        if (oracle_lemire32_accept(w[q], bound, &out)) return out;
+    return (uint32_t)(((uint64_t)w[0] * bound) >> 32);
+}
+
+uint32_t oracle_ipsc_depth(uint64_t m, uint32_t k)
+{
+    const uint64_t n0 = (uint64_t)k * k;
+    uint32_t t = 0;
+    while (t < IPSC_TMAX && (m >> (t + 1)) >= n0) ++t;
+    return t;
+}
+
+typedef struct {
+    unsigned char *A;
+    uint32_t eb, k, L;
+    uint64_t K;
+    uint32_t max_levels;
+    int run_leaves;
+    uint64_t *b, *s, *e;   /* scratch triples: nodes x k (node v at index (v-1) * k) */
+    oracle_ipsc_stats *st;
+    uint64_t *sizes0;      /* optional: the root segment's final bucket sizes */
+} ipsc_ctx;
+
+static void ipsc_swap(ipsc_ctx *c, uint64_t x, uint64_t y)
+{
+    if (x != y) elem_swap(c->A + x * c->eb, c->A + y * c->eb, c->eb);
+}
+
+/* RoughScatter on node v's triples. */
+static void ipsc_rough(ipsc_ctx *c, uint64_t *b, uint64_t *s, uint64_t *e, uint32_t v, uint32_t level, uint64_t a)
+{
+    (void)b;
+    for (uint32_t i = 0; i < c->k; ++i)
+        if (s[i] == e[i]) return; /* a full bucket: nothing to do */
+    for (uint32_t step = 0;; ++step) {
+        const uint32_t j = oracle_ipsc_draw(c->K, IPSC_RS, step, v, level, a, c->k);
+        if (j != 0) ipsc_swap(c, s[0], s[j]);
+        s[j] += 1;
+        if (c->st) c->st->rough_steps += 1;
+        if (s[j] == e[j]) return;
+    }
+}
+
+/* Node v (depth d of t) over bucket ranges [lo_i, hi_i): result triples in node v's slot. */
+static void ipsc_node(ipsc_ctx *c, uint32_t v, uint32_t d, uint32_t t, const uint64_t *lo, const uint64_t *hi,
+                      uint32_t level, uint64_t a)
+{
+    const uint32_t k = c->k;
+    uint64_t *b = c->b + (uint64_t)(v - 1) * k, *s = c->s + (uint64_t)(v - 1) * k, *e = c->e + (uint64_t)(v - 1) * k;
+    if (d == t) {
+        for (uint32_t i = 0; i < k; ++i) {
+            b[i] = lo[i];
+            s[i] = lo[i];
+            e[i] = hi[i];
+        }
+    } else {
+        uint64_t *mid = (uint64_t *)calloc((size_t)k, sizeof(uint64_t));
+        if (!mid) abort();
+        for (uint32_t i = 0; i < k; ++i) mid[i] = lo[i] + (hi[i] - lo[i]) / 2;
+        ipsc_node(c, 2 * v, d + 1, t, lo, mid, level, a);
+        ipsc_node(c, 2 * v + 1, d + 1, t, mid, hi, level, a);
+        free(mid);
+        const uint64_t *b1 = c->b + (uint64_t)(2 * v - 1) * k, *s1 = c->s + (uint64_t)(2 * v - 1) * k,
+                       *e1 = c->e + (uint64_t)(2 * v - 1) * k;
+        const uint64_t *b2 = c->b + (uint64_t)(2 * v) * k, *s2 = c->s + (uint64_t)(2 * v) * k,
+                       *e2 = c->e + (uint64_t)(2 * v) * k;
+        for (uint32_t i = 0; i < k; ++i) {
+            const uint64_t A = e1[i] - s1[i], B = s2[i] - b2[i], mn = A < B ? A : B;
+            for (uint64_t x = 0; x < mn; ++x) ipsc_swap(c, s1[i] + x, s2[i] - 1 - x);
+            if (c->st) c->st->merge_swaps += mn;
+            b[i] = b1[i];
+            s[i] = s1[i] + B;
+            e[i] = e2[i];
+        }
+    }
+    ipsc_rough(c, b, s, e, v, level, a);
+}
+
+/* FineScatter at the root; writes the final bucket sizes to nf. */
+static int ipsc_fine(ipsc_ctx *c, uint64_t *b, uint64_t *s, uint64_t *e, uint64_t *nf, uint32_t level, uint64_t a)
+{
+    const uint32_t k = c->k;
+    uint64_t R = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+        R += e[i] - s[i];
+        nf[i] = s[i] - b[i];
+    }
+    if (R > 0xFFFFFFFFull) return ORACLE_ERR_INVALID_ARG;
+    for (uint64_t r = 0; r < R; ++r) nf[oracle_ipsc_draw(c->K, IPSC_FM, (uint32_t)r, 0u, level, a, k)] += 1;
+    {   /* Lemma 4: sum_i |D_i| from the capacities and the final sizes (the TwoSweep count below must match) */
+        int64_t D = 0;
+        for (uint32_t i = 0; i < k; ++i) {
+            D += (int64_t)nf[i] - (int64_t)(e[i] - b[i]);
+            if (c->st) c->st->dsum += (uint64_t)(D < 0 ? -D : D);
+        }
+    }
+    /* TwoSweep: D_i = sum_{j<=i} (n^f_j - c_j); across the boundary of
+     * buckets i and i+1, -D_i > 0 items move right in the ascending sweep (the
+     * excess of B_i beyond what the buckets left of it still need, C_i) and
+     * D_i > 0 items move left in the descending sweep: sum_i |D_i| transfers. */
+    int64_t *Dp = (int64_t *)malloc((size_t)k * sizeof(int64_t));
+    if (!Dp) return ORACLE_ERR_NOMEM;
+    {
+        int64_t D = 0;
+        for (uint32_t i = 0; i < k; ++i) {
+            D += (int64_t)nf[i] - (int64_t)(e[i] - b[i]);
+            Dp[i] = D;
+        }
+    }
+    for (uint32_t i = 0; i + 1 < k; ++i) /* sweep 1: B_i's last staged slot -> B_{i+1} */
+        for (int64_t x = -Dp[i]; x > 0; --x) {
+            e[i] -= 1;
+            b[i + 1] -= 1;
+            if (s[i + 1] > b[i + 1] + 1) ipsc_swap(c, b[i + 1], s[i + 1] - 1);
+            s[i + 1] -= 1;
+            if (c->st) c->st->transfers += 1;
+        }
+    for (uint32_t i = k - 1; i-- > 0;) /* sweep 2: B_{i+1}'s first slot -> B_i */
+        for (int64_t x = Dp[i]; x > 0; --x) {
+            if (s[i + 1] > b[i + 1]) ipsc_swap(c, b[i + 1], s[i + 1]);
+            b[i + 1] += 1;
+            s[i + 1] += 1;
+            e[i] += 1;
+            if (c->st) c->st->transfers += 1;
+        }
+    free(Dp);
+    for (uint32_t i = 0; i < k; ++i)
+        if (e[i] - b[i] != nf[i] || s[i] > e[i] || s[i] < b[i]) return ORACLE_ERR_INVALID_ARG; /* internal */
+    /* stash shuffle: compact, Fisher-Yates, undo */
+    uint64_t t = 0;
+    for (uint32_t i = 0; i < k; ++i)
+        for (uint64_t p = s[i]; p < e[i]; ++p) ipsc_swap(c, a + t++, p);
+    for (uint64_t i = R; i-- > 1;)
+        ipsc_swap(c, a + i, a + oracle_ipsc_draw(c->K, IPSC_FY, (uint32_t)i, 0u, level, a, (uint32_t)(i + 1)));
+    for (uint32_t i = k; i-- > 0;)
+        for (uint64_t p = e[i]; p-- > s[i];) ipsc_swap(c, a + --t, p);
+    if (c->st) c->st->staged += R;
+    return 0;
+}
+
+static int ipsc_rec(ipsc_ctx *c, uint64_t a, uint64_t m, uint32_t level)
+{
+    if (m <= c->L) {
+        if (c->run_leaves && m >= 2) {
+            for (uint64_t i = m; i-- > 1;) {
+                const uint32_t j = oracle_fy_draw(c->K, a, (uint32_t)i, NULL);
+                ipsc_swap(c, a + i, a + j);
+            }
+            if (c->st) c->st->leaves += 1;
+        }
+        return 0;
+    }
+    if (level >= c->max_levels) return 0;
+    if (level > 255) return ORACLE_ERR_DEPTH;
+    const uint32_t k = c->k, t = oracle_ipsc_depth(m, k);
+    uint64_t *lo = (uint64_t *)malloc((size_t)k * sizeof(uint64_t)), *hi = (uint64_t *)malloc((size_t)k * sizeof(uint64_t));
+    uint64_t *nf = (uint64_t *)malloc((size_t)k * sizeof(uint64_t));
+    if (!lo || !hi || !nf) return ORACLE_ERR_NOMEM;
+    for (uint32_t i = 0; i < k; ++i) {
+        lo[i] = a + (uint64_t)(((unsigned __int128)i * m) / k);
+        hi[i] = a + (uint64_t)(((unsigned __int128)(i + 1) * m) / k);
+    }
+    ipsc_node(c, 1, 0, t, lo, hi, level, a);
+    int rc = ipsc_fine(c, c->b, c->s, c->e, nf, level, a);
+    if (c->st) c->st->segments += 1;
+    if (!rc && level == 0 && c->sizes0) memcpy(c->sizes0, nf, (size_t)k * sizeof(uint64_t));
+    free(lo);
+    free(hi);
+    uint64_t start = a;
+    for (uint32_t i = 0; i < k && !rc; ++i) {
+        rc = ipsc_rec(c, start, nf[i], level + 1);
+        start += nf[i];
+    }
+    free(nf);
+    return rc;
+}
+
+int oracle_ipsc_shuffle(void *data, uint64_t n, uint32_t eb, uint32_t k, uint32_t L, uint64_t seed,
+                        uint32_t max_levels, int run_leaves, oracle_ipsc_stats *st, uint64_t *sizes0)
+{
+    if (eb == 0 || k < 2 || k > 65536u || L < 1 || n >= (1ull << 48)) return ORACLE_ERR_INVALID_ARG;
+    ipsc_ctx c;
+    memset(&c, 0, sizeof c);
+    c.A = (unsigned char *)data;
+    c.eb = eb;
+    c.k = k;
+    c.L = L;
+    c.K = oracle_problem_key(seed, 0);
+    c.max_levels = max_levels;
+    c.run_leaves = run_leaves;
+    c.st = st;
+    c.sizes0 = sizes0;
+    if (st) memset(st, 0, sizeof *st);
+    const uint64_t nodes = 2ull << oracle_ipsc_depth(n, k);  /* the root segment needs the deepest tree */
+    c.b = (uint64_t *)malloc(nodes * k * sizeof(uint64_t));
+    c.s = (uint64_t *)malloc(nodes * k * sizeof(uint64_t));
+    c.e = (uint64_t *)malloc(nodes * k * sizeof(uint64_t));
+    int rc = (!c.b || !c.s || !c.e) ? ORACLE_ERR_NOMEM : ipsc_rec(&c, 0, n, 0);
+    free(c.b);
+    free(c.s);
+    free(c.e);
+    return rc;
+}

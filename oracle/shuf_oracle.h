@@ -37,4 +37,21 @@ int oracle_points(uint64_t n, uint32_t k, uint32_t L, uint64_t seed, const uint6
                   uint64_t *out);
 int oracle_sim_rough_scatter(uint64_t n, uint32_t k, uint64_t seed, uint32_t runs, uint64_t *T, uint64_t *M);
 
+/* D10 (NEXT-2): the paper's In-Place ScatterShuffle (RoughScatter, ParRoughScatter
+ * merges, FineScatter with TwoSweep and the stash shuffle), deterministic draws. */
+typedef struct {
+    uint64_t segments;     /* IpSc segments processed                          */
+    uint64_t rough_steps;  /* RoughScatter iterations (all nodes)              */
+    uint64_t merge_swaps;  /* ParRoughScatter merge swaps                      */
+    uint64_t staged;       /* sum of R (items left staged for FineScatter)     */
+    uint64_t transfers;    /* TwoSweep unit transfers                          */
+    uint64_t dsum;         /* sum over segments of sum_i |D_i| (Lemma 4)       */
+    uint64_t leaves;       /* Fisher-Yates leaves                              */
+} oracle_ipsc_stats;
+uint32_t oracle_ipsc_draw(uint64_t K, uint32_t tag, uint32_t c0, uint32_t c1, uint32_t level, uint64_t a,
+                          uint32_t bound);
+uint32_t oracle_ipsc_depth(uint64_t m, uint32_t k);
+int oracle_ipsc_shuffle(void *data, uint64_t n, uint32_t eb, uint32_t k, uint32_t L, uint64_t seed,
+                        uint32_t max_levels, int run_leaves, oracle_ipsc_stats *st, uint64_t *sizes0);
+
 #endif
