@@ -182,6 +182,84 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, w, rank, world, local, dev):
+    """--mode sharded (NEXT-3): ONE problem of N = world * n
+    elements (the workload's shape per rank, weak scaling), rank r holding
+    global positions [rN/world, (r+1)N/world); a step = level-0 scatter of
+    the slice, count all-gather, the all-to-all-v of the bucket pieces (NCCL
+    grouped send/recv), D6 from level 1 on the owned buckets.  Same input
+    slice every step (the scatter reads it, the output goes elsewhere)."""
+    import torch
+    from paper_2302_03317_b200 import sharded
+    import paper_2302_03317_b200 as shuf
+    if w.kind == "segmented":
+        raise SystemExit("--mode sharded: single-shuffle workloads only")
+    N = w.n * world
+    st = sharded.ShardedShuffle(N, w.elem_bytes, w.k, w.L, w.seed, rank, world, dev)
+    m = st.hi - st.lo
+    if w.elem_bytes == 4:
+        x = torch.arange(st.lo, st.hi, dtype=torch.int64, device=dev).to(torch.int32)
+    else:
+        x = synth.make_input_torch(synth.Workload(w.name, m, w.elem_bytes, w.k, w.L, w.seed, w.kind,
+                                                  w.num_segments, w.note), dev)
+    stream = torch.cuda.current_stream(dev)
+    p2p = sharded.torch_p2p()
+    info = {}
+
+    def step():
+        st.scatter(x, stream)
+        if st.degenerate:
+            ex = st.degenerate_plan()
+        elif world > 1:
+            ex = sharded.exchange_plan(sharded.all_gather_counts(st.counts, world), world, w.k, rank)
+        else:
+            ex = sharded.exchange_plan([st.counts.cpu().tolist()], 1, w.k, 0)
+        launches = shuf.shuf_last_launch_count(st.plan)
+        st.exchange(ex, p2p)
+        st.finish(ex, stream)
+        info.update(m=ex.m, base=ex.base, pieces=len(ex.sends) + len(ex.recvs),
+                    launches=launches + shuf.shuf_last_launch_count(st.plan))
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    err = shuf.shuf_last_device_error(st.plan, stream)
+    if err:
+        raise SystemExit(f"device error {err}")
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
+    value = N / (ms / 1e3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": DTYPE[w.elem_bytes], "data": "synthetic",
+            "config": {"workload": f"{args.workload} x{world} as ONE sharded problem: N={N}, k={w.k}, L={w.L}, "
+                                   f"seed={w.seed}", "n": N, "elem_bytes": w.elem_bytes, "k": w.k, "L": w.L,
+                       "seed": w.seed, "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"sharded x{world} (level-0 all-to-all-v over NCCL)", "mode": "sharded",
+                       "rank0_owned": info.get("m"), "rank0_p2p_pieces": info.get("pieces")},
+            "e2e": None, "roofline": None, "cpu_baseline": None,
+            "gpu_launches": info.get("launches", 0) * args.steps, "clocks": clk.summary(), "device": device_facts(dev),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -219,8 +297,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="hot", choices=["hot", "c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--mode", default="stable", choices=["stable", "inplace"],
-                    help="inplace: shuf_run_inplace (SURVEY 8(a) a10; aux memory instead of the ping-pong buffer)")
+    ap.add_argument("--mode", default="stable", choices=["stable", "inplace", "sharded"],
+                    help="inplace: shuf_run_inplace (SURVEY 8(a) a10; aux memory instead of the ping-pong buffer); "
+                         "sharded: ONE problem of N x n elements split over the N ranks (NEXT-3, one level-0 "
+                         "all-to-all-v over NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 25)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
@@ -244,6 +324,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     w = synth.WORKLOADS[args.workload]
+    if args.mode == "sharded":
+        return run_sharded(args, w, rank, world, local, dev)
     seed = rank_seed(w.seed, rank)
     if w.kind == "segmented":
         lens = synth.c5_lengths(w.num_segments, w.seed)

@@ -101,6 +101,41 @@ shuf_status shuf_run(shuf_plan_t p, void *ptr, void *scratch, uint64_t scratch_b
 shuf_status shuf_segmented(shuf_plan_t p, void *ptr, const uint64_t *d_offsets, uint64_t num_segments,
                            void *scratch, uint64_t scratch_bytes, void *stream);
 
+/* Sharded single shuffle (data sets approaching memory
+ * size, P:9).  ONE problem of N elements (D6 with K = seed) is split over G
+ * ranks: rank r holds the global positions [lo_r, hi_r).  D6's level 0 is the
+ * only step that crosses ranks (the stable bucket grouping of the
+ * whole array); every later level and leaf stays inside one bucket.
+ *   1. shuf_shard_scatter: the rank's slice in[0..m) (global positions
+ *      [pos0, pos0+m)) is grouped by its level-0 draws, stably, into out[0..m)
+ *      (bucket-major, position order inside a bucket) and d_counts[b] (DEVICE,
+ *      k uint64) receives the slice's count of bucket b.  The slice is
+ *      scattered whatever its length: the caller only shards problems with
+ *      N > L (otherwise D6 has no level 0 and the whole array is one leaf).
+ *   2. The caller exchanges the runs (all-to-all-v over NCCL,
+ *      paper_2302_03317_b200/sharded.py): bucket b's final place in the
+ *      global level-0 output is o_b + sum over source ranks s' < s of their
+ *      counts of b, so an owner of buckets [b0, b1) receives them in
+ *      (bucket, source rank) order -- exactly D6's stable order.
+ *   3. shuf_shard_continue: ptr[0..m) holds global positions [base, base+m)
+ *      of the level-first_level input, cut into num_segments consecutive
+ *      segments d_offsets[0..num_segments] (DEVICE, ascending, 0 .. m), each
+ *      a child (bucket) at level first_level (= 1) of the one problem: D6
+ *      continues on each with key K(seed, 0) and global positions, in place.
+ * The concatenation of all ranks' ptr is D6's output of the whole problem,
+ * bit for bit.  The plan's n is a CAPACITY: m <= n for both calls (its level
+ * count and chunk size come from n).  scratch: shuf_scratch_bytes_shard bytes
+ * (16-byte aligned), one buffer serves both calls; in/out/ptr 16-byte aligned;
+ * elem_bytes must be 4, 8 or 16 (else SHUF_ERR_UNSUPPORTED).  Stream-ordered,
+ * no host synchronisation, no allocation; device errors via
+ * shuf_last_device_error. */
+shuf_status shuf_scratch_bytes_shard(shuf_plan_t p, uint64_t *bytes);
+shuf_status shuf_shard_scatter(shuf_plan_t p, const void *in, uint64_t m, uint64_t pos0, void *out,
+                               uint64_t *d_counts, void *scratch, uint64_t scratch_bytes, void *stream);
+shuf_status shuf_shard_continue(shuf_plan_t p, void *ptr, uint64_t m, const uint64_t *d_offsets,
+                                uint64_t num_segments, uint64_t base, uint32_t first_level, void *scratch,
+                                uint64_t scratch_bytes, void *stream);
+
 /* In-place mode (the paper's in-place motivation P:32-36,
  * P:39-43).  Shuffles ptr[0..n) using an auxiliary DEVICE buffer `aux` of
  * shuf_aux_bytes_inplace() bytes, about 2 bytes per 128-byte block of ptr plus

@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = [
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
     "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks", "shuf_aux_bytes_inplace", "shuf_run_inplace",
+    "shuf_scratch_bytes_shard", "shuf_shard_scatter", "shuf_shard_continue",
     "shuf_debug_inplace_levels", "shuf_scratch_bytes_segmented", "shuf_sim_rough_scatter",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish", "leaf"]
@@ -100,6 +101,12 @@ def lib():
         L.shuf_debug_inplace_levels.argtypes = [vp, vp, vp, u64, vp, u32, i32]
         L.shuf_debug_inplace_levels.restype = i32
         L.shuf_rank_mode.restype = i32
+        L.shuf_scratch_bytes_shard.argtypes = [vp, ctypes.POINTER(u64)]
+        L.shuf_scratch_bytes_shard.restype = i32
+        L.shuf_shard_scatter.argtypes = [vp, vp, u64, u64, vp, vp, vp, u64, vp]
+        L.shuf_shard_scatter.restype = i32
+        L.shuf_shard_continue.argtypes = [vp, vp, u64, vp, u64, u64, u32, vp, u64, vp]
+        L.shuf_shard_continue.restype = i32
         L.shuf_status_string.argtypes = [i32]
         L.shuf_status_string.restype = ctypes.c_char_p
         _lib = L
@@ -202,6 +209,44 @@ def shuf_segmented(plan: Plan, x, d_offsets, scratch, stream=None):
     _check(lib().shuf_segmented(plan.handle, _dev_ptr(x, "x"), _dev_ptr(d_offsets, "offsets"), d_offsets.numel() - 1,
                                 _dev_ptr(scratch, "scratch"), scratch.numel() * scratch.element_size(),
                                 _stream(stream)), "shuf_segmented", plan)
+
+
+def shuf_scratch_bytes_shard(plan: Plan) -> int:
+    b = ctypes.c_uint64(0)
+    _check(lib().shuf_scratch_bytes_shard(plan.handle, ctypes.byref(b)), "shuf_scratch_bytes_shard", plan)
+    return int(b.value)
+
+
+def _check_slice(plan: Plan, x, m: int, what: str):
+    if x.numel() * x.element_size() < m * plan.elem_bytes:
+        raise ValueError(f"{what} holds fewer than m = {m} elements")
+
+
+def shuf_shard_scatter(plan: Plan, x, m: int, pos0: int, out, d_counts, scratch, stream=None):
+    """Sharded level 0 (include/shuf.h): x[0..m) at global positions pos0.. grouped
+    stably by bucket into out[0..m); d_counts (k int64, device) the slice's counts."""
+    import torch
+    _check_slice(plan, x, m, "x")
+    _check_slice(plan, out, m, "out")
+    if d_counts.dtype not in (torch.int64, torch.uint64) or d_counts.numel() < plan.k:
+        raise ValueError("d_counts must be a 64-bit CUDA tensor of k entries")
+    _check(lib().shuf_shard_scatter(plan.handle, _dev_ptr(x, "x"), m, pos0, _dev_ptr(out, "out"),
+                                    _dev_ptr(d_counts, "d_counts"), _dev_ptr(scratch, "scratch"),
+                                    scratch.numel() * scratch.element_size(), _stream(stream)),
+           "shuf_shard_scatter", plan)
+
+
+def shuf_shard_continue(plan: Plan, x, m: int, d_offsets, base: int, first_level: int, scratch, stream=None):
+    """Sharded continuation (include/shuf.h): x[0..m) = global positions base..,
+    segments d_offsets (device, int64) are children at first_level; D6 in place."""
+    import torch
+    _check_slice(plan, x, m, "x")
+    if d_offsets.dtype not in (torch.int64, torch.uint64):
+        raise ValueError("offsets must be a 64-bit CUDA tensor")
+    _check(lib().shuf_shard_continue(plan.handle, _dev_ptr(x, "x"), m, _dev_ptr(d_offsets, "offsets"),
+                                     d_offsets.numel() - 1, base, first_level, _dev_ptr(scratch, "scratch"),
+                                     scratch.numel() * scratch.element_size(), _stream(stream)),
+           "shuf_shard_continue", plan)
 
 
 def shuf_aux_bytes_inplace(plan: Plan) -> int:

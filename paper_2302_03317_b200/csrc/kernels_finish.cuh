@@ -656,13 +656,13 @@ struct SegIter {
                 const uint64_t a = off[si], b = off[si + 1];
                 if (b <= a || b - a > rp->S_fuse) continue;
                 if (rp->leafk && b - a <= rp->L) continue;  // the leaf kernel's
-                if (!item_permutes(*rp, (uint32_t)(b - a), 0u)) continue;
+                if (!item_permutes(*rp, (uint32_t)(b - a), rp->first_level)) continue;
                 Item& it = ctl->items[slot];
                 it.start = a;
                 it.len = (uint32_t)(b - a);
-                it.level = 0;
-                it.origin = a;
-                it.key = rp->seed + si * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
+                it.level = rp->first_level;
+                it.origin = rp->shard ? 0ull - rp->seg_base : a;
+                it.key = rp->shard ? rp->seed : rp->seed + si * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
                 ctl->have[slot] = 1;
                 break;
             }

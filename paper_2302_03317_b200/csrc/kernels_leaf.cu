@@ -140,6 +140,8 @@ struct SegLeaves {
     const uint64_t* off;
     uint64_t nsegs, seed;
     uint32_t U;
+    uint32_t shard;     // RunParams::shard: key K(seed, 0), origin -base
+    uint64_t base;
     __device__ __forceinline__ uint64_t units() const { return (nsegs + U - 1) / U; }
     __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
         Leaf f{0, 0, 0, 0};
@@ -148,8 +150,8 @@ struct SegLeaves {
             f.start = off[s];
             const uint64_t e = off[s + 1];
             f.len = e > f.start ? e - f.start : 0;
-            f.origin = f.start;
-            f.key = seed + s * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
+            f.origin = shard ? 0ull - base : f.start;
+            f.key = shard ? seed : seed + s * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
         }
         return f;
     }
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_children(RunParams rp, Le
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_segments(RunParams rp, const uint64_t* __restrict__ off,
                                                                  uint64_t nsegs, uint32_t U) {
-    const SegLeaves ls{off, nsegs, rp.seed, U};
+    const SegLeaves ls{off, nsegs, rp.seed, U, rp.shard, rp.seg_base};
     run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
 }
 

@@ -67,13 +67,48 @@ __global__ void k_init_segmented(RunParams rp, LevelParams lp0, const uint64_t* 
         SegDesc sd;
         sd.start = a;
         sd.len = len;
-        sd.origin = a;
-        sd.key = rp.seed + s * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
+        // user segment s: K(seed, s), positions segment-relative (D7); a sharded
+        // rank's level-0 children: K(seed, 0), global positions (NEXT-3)
+        sd.origin = rp.shard ? 0ull - rp.seg_base : a;
+        sd.key = rp.shard ? rp.seed : rp.seed + s * 0x9E3779B97F4A7C15ull;
         sd.cbase = (uint64_t)cb * rp.k;
         sd.nchunks = (uint32_t)nch;
         sd.pad = 0;
         lp0.segs[si] = sd;
         for (uint64_t c = 0; c < nch; ++c) lp0.chunks[cb + c] = ChunkDesc{si, (uint32_t)c};
+    }
+}
+
+// Sharded level 0 (NEXT-3): the rank's input slice [0, m) holds the global
+// level-0 positions [pos0, pos0 + m) of the one problem (K(seed, 0)); it is
+// scattered as one segment whatever its length (the whole problem exceeds L).
+__global__ void k_init_shard(RunParams rp, LevelParams lp0, uint64_t m, uint64_t pos0) {
+    const uint64_t nch = (m + rp.chunk - 1) / rp.chunk;
+    if (gtid() == 0) {
+        SegDesc sd;
+        sd.start = 0;
+        sd.len = m;
+        sd.origin = 0ull - pos0;
+        sd.key = rp.seed;  // K(seed, 0) (D2)
+        sd.cbase = 0;
+        sd.nchunks = (uint32_t)nch;
+        sd.pad = 0;
+        lp0.segs[0] = sd;
+        lp0.ctr->nseg = 1;
+        lp0.ctr->nchunk = (uint32_t)nch;
+        if (nch > lp0.max_chunks) latch_error(rp.hdr, 4u /*SHUF_ERR_SCRATCH*/);
+    }
+    for (uint64_t j = gtid(); j < nch && j < lp0.max_chunks; j += gstride()) lp0.chunks[j] = ChunkDesc{0u, (uint32_t)j};
+}
+
+// counts[b] = |child b| of the sharded level-0 segment (after k_scan).
+__global__ void k_shard_counts(RunParams rp, LevelParams lp, uint64_t* __restrict__ counts) {
+    const SegDesc sg = lp.segs[0];
+    const uint64_t base0 = lp.prefix[sg.cbase];
+    for (uint64_t b = gtid(); b < rp.k; b += gstride()) {
+        const uint64_t s0 = lp.prefix[sg.cbase + b * sg.nchunks] - base0;
+        const uint64_t s1 = (b + 1 < rp.k) ? lp.prefix[sg.cbase + (b + 1) * sg.nchunks] - base0 : sg.len;
+        counts[b] = s1 - s0;
     }
 }
 
@@ -303,6 +338,17 @@ cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_
 cudaError_t launch_init_segmented(const RunParams& rp, const LevelParams& lp0, const uint64_t* d_offsets,
                                   uint64_t num_segments, cudaStream_t s, int grid) {
     k_init_segmented<<<grid, 256, 0, s>>>(rp, lp0, d_offsets, num_segments);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_shard(const RunParams& rp, const LevelParams& lp0, uint64_t m, uint64_t pos0, cudaStream_t s,
+                              int grid) {
+    k_init_shard<<<grid, 256, 0, s>>>(rp, lp0, m, pos0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_counts(const RunParams& rp, const LevelParams& lp, uint64_t* counts, cudaStream_t s) {
+    k_shard_counts<<<(rp.k + 255) / 256, 256, 0, s>>>(rp, lp, counts);
     return cudaGetLastError();
 }
 

@@ -545,21 +545,36 @@ struct Prof {
         ++launches;                                         \
     } while (0)
 
-// Enqueue the whole shuffle.  segmented: d_offsets != nullptr.
-static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets, uint64_t nsegs, void* scratch,
-                           cudaStream_t st, uint32_t max_levels, int run_leaves, Prof* prof = nullptr) {
-    p->last_launches = 0;
-    cudaError_t e = device_setup(p);
-    if (e) return cuda_fail(p, e);
-    unsigned char* sc = static_cast<unsigned char*>(scratch);
-    unsigned char* buf0 = static_cast<unsigned char*>(ptr);
-    const ScratchLayout lay = d_offsets ? compute_layout(p, seg0_bound(p, nsegs), true) : p->lay;
-    Header* hdr = reinterpret_cast<Header*>(sc + lay.header);
-    p->last_hdr = hdr;
-    RunParams rp;
+// A sharded rank's slice (NEXT-3): n elements at global positions [base, ..),
+// segments that are children at first_level of the one problem, laid out in
+// the plan's shard layout (shard_layout).
+struct ShardOpts {
+    uint64_t n, base;
+    uint32_t first_level;
+    ScratchLayout lay;
+};
+
+// Layout shared by shuf_shard_scatter (one level-0 slice of <= n elements) and
+// shuf_shard_continue (<= k segments of <= n elements in total).
+static ScratchLayout shard_layout(const shuf_plan_s* p) {
+    shuf_plan_s q = *p;
+    if (q.levels < 1) q.levels = 1;
+    return compute_layout(&q, seg0_bound(&q, p->k), true);
+}
+
+extern "C" shuf_status shuf_scratch_bytes_shard(shuf_plan_t p, uint64_t* bytes) {
+    if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) return SHUF_ERR_UNSUPPORTED;
+    *bytes = shard_layout(p).total;
+    return SHUF_OK;
+}
+
+static RunParams base_params(const shuf_plan_s* p, const ScratchLayout& lay, unsigned char* sc, unsigned char* buf0,
+                             uint32_t max_levels, int run_leaves) {
+    RunParams rp{};
     rp.buf0 = buf0;
     rp.buf1 = sc + lay.pingpong;
-    rp.hdr = hdr;
+    rp.hdr = reinterpret_cast<Header*>(sc + lay.header);
     rp.n = p->n;
     rp.eb = p->eb;
     rp.k = p->k;
@@ -584,6 +599,31 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         rp.dbg = dbg ? (uint32_t)std::atoi(dbg) : 0u;
     }
     rp.flags = sc + lay.flags;
+    return rp;
+}
+
+// Enqueue the whole shuffle.  segmented: d_offsets != nullptr; a sharded
+// rank's continuation: so != nullptr (with d_offsets).
+static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets, uint64_t nsegs, void* scratch,
+                           cudaStream_t st, uint32_t max_levels, int run_leaves, Prof* prof = nullptr,
+                           const ShardOpts* so = nullptr) {
+    p->last_launches = 0;
+    cudaError_t e = device_setup(p);
+    if (e) return cuda_fail(p, e);
+    unsigned char* sc = static_cast<unsigned char*>(scratch);
+    unsigned char* buf0 = static_cast<unsigned char*>(ptr);
+    const ScratchLayout lay = so ? so->lay : d_offsets ? compute_layout(p, seg0_bound(p, nsegs), true) : p->lay;
+    Header* hdr = reinterpret_cast<Header*>(sc + lay.header);
+    p->last_hdr = hdr;
+    RunParams rp = base_params(p, lay, sc, buf0, max_levels, run_leaves);
+    const uint32_t lv0 = so ? so->first_level : 0u;
+    if (so) {
+        rp.n = so->n;
+        rp.shard = 1;
+        rp.first_level = lv0;
+        rp.seg_base = so->base;
+        rp.planned_levels = p->levels + lv0;
+    }
     uint64_t launches = 0;
     if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
     const LevelParams lp0 = level_params(lay, sc, buf0, 0, true);
@@ -598,15 +638,17 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
             else LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, hdr->root_off, 1, st, 1));
         }
     }
-    const uint32_t G = p->levels < max_levels ? p->levels : max_levels;
+    const uint32_t lim = max_levels > lv0 ? max_levels - lv0 : 0u;
+    const uint32_t G = p->levels < lim ? p->levels : lim;
     // level l+1's histogram needs only k_plan(l)'s list, so it is forked onto
     // the side stream before level l's scatter and joined before scan(l+1)
     // (fork/join inside the call: still stream-ordered for the caller)
     const bool overlap = p->hist_overlap && !prof;
     for (uint32_t lv = 0; lv < G; ++lv) {
         LevelParams lp = level_params(lay, sc, buf0, lv);
+        lp.level = lv + lv0;  // draws are keyed by the problem's level; buffers and slots by lv
         {  // expected child length of the level: (n / segments) / k^(lv+1)
-            double avg = (double)p->n / (double)(d_offsets ? (nsegs ? nsegs : 1) : 1);
+            double avg = (double)rp.n / (double)(d_offsets ? (nsegs ? nsegs : 1) : 1);
             for (uint32_t i = 0; i <= lv; ++i) avg /= (double)p->k;
             lp.leaf_unit = leaf_unit(p->eb, p->L, (uint64_t)avg);
         }
@@ -620,14 +662,16 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         if (overlap && lv + 1 < G) {
             if ((e = cudaEventRecord(p->ev_fork, st))) return cuda_fail(p, e);
             if ((e = cudaStreamWaitEvent(p->side_stream, p->ev_fork, 0))) return cuda_fail(p, e);
-            LAUNCH(SHUF_K_HIST, launch_hist(rp, level_params(lay, sc, buf0, lv + 1), p->side_stream, p->grid_hist));
+            LevelParams ln = level_params(lay, sc, buf0, lv + 1);
+            ln.level = lv + 1 + lv0;
+            LAUNCH(SHUF_K_HIST, launch_hist(rp, ln, p->side_stream, p->grid_hist));
             if ((e = cudaEventRecord(p->ev_join, p->side_stream))) return cuda_fail(p, e);
         }
         LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
         if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast(rp, lp, st, p->grid_fast));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
         if (p->leafk) LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->grid_leaf));
-        if (lv + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
+        if (lv + lv0 + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
     }
     // leaves of the recorded fused items (all levels; they sit in ptr)
     if (p->defer && (d_offsets || p->n > p->L)) LAUNCH(SHUF_K_LEAF, launch_leaf_items(rp, st, p->grid_leaf));
@@ -919,6 +963,77 @@ extern "C" shuf_status shuf_segmented(shuf_plan_t p, void* ptr, const uint64_t* 
         return gather_route(p, ptr, d_offsets, num_segments, scratch, scratch_bytes, static_cast<cudaStream_t>(stream),
                             0xFFFFFFFFu, 1, nullptr);
     return enqueue(p, ptr, d_offsets, num_segments, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
+}
+
+// ------------------------------------------------------------- sharded ---
+// NEXT-3: one problem of N elements sharded over ranks.  Rank r
+// scatters its input slice at level 0 (shuf_shard_scatter), the runs of each
+// bucket go to the bucket's owner (the caller's exchange, NCCL), and every
+// owner finishes its buckets as level-1 segments (shuf_shard_continue).
+static shuf_status check_shard_args(shuf_plan_s* p, const void* a, const void* b, void* scratch,
+                                    uint64_t scratch_bytes, uint64_t m) {
+    if (!p) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) return SHUF_ERR_UNSUPPORTED;  // elem_bytes in {4, 8, 16}
+    if (m > p->n) return SHUF_ERR_INVALID_ARG;
+    if (m && (!a || !b || !scratch)) return SHUF_ERR_INVALID_ARG;
+    if (((uintptr_t)a & 15u) || ((uintptr_t)b & 7u) || ((uintptr_t)scratch & 15u)) return SHUF_ERR_ALIGNMENT;
+    if (m && scratch_bytes < shard_layout(p).total) return SHUF_ERR_SCRATCH;
+    return SHUF_OK;
+}
+
+extern "C" shuf_status shuf_shard_scatter(shuf_plan_t p, const void* in, uint64_t m, uint64_t pos0, void* out,
+                                          uint64_t* d_counts, void* scratch, uint64_t scratch_bytes, void* stream) {
+    shuf_status s = check_shard_args(p, in, d_counts, scratch, scratch_bytes, m);
+    if (s) return s;
+    if (m && (!out || ((uintptr_t)out & 15u))) return out ? SHUF_ERR_ALIGNMENT : SHUF_ERR_INVALID_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = device_setup(p);
+    if (e) return cuda_fail(p, e);
+    if (m == 0) {
+        if (d_counts && (e = cudaMemsetAsync(d_counts, 0, (size_t)p->k * 8, st))) return cuda_fail(p, e);
+        p->last_launches = 0;
+        return SHUF_OK;
+    }
+    unsigned char* sc = static_cast<unsigned char*>(scratch);
+    unsigned char* buf0 = static_cast<unsigned char*>(const_cast<void*>(in));
+    const ScratchLayout lay = shard_layout(p);
+    RunParams rp = base_params(p, lay, sc, buf0, 1u, 0);
+    rp.n = m;
+    rp.shard = 1;
+    rp.seg_base = pos0;
+    rp.planned_levels = 1;
+    p->last_hdr = rp.hdr;
+    uint64_t launches = 0;
+    Prof* prof = nullptr;
+    if ((e = cudaMemsetAsync(rp.hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
+    LAUNCH(SHUF_K_INIT, launch_init_shard(rp, level_params(lay, sc, buf0, 0, true), m, pos0, st, p->grid_small));
+    LevelParams lp = level_params(lay, sc, buf0, 0);
+    lp.dst = static_cast<unsigned char*>(out);
+    LAUNCH(SHUF_K_HIST, launch_hist(rp, lp, st, p->grid_hist));
+    LAUNCH(SHUF_K_SCAN, launch_scan(rp, lp, st, p->grid_scan));
+    LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
+    LAUNCH(SHUF_K_PLAN, launch_shard_counts(rp, lp, d_counts, st));
+    p->last_launches = launches;
+    return SHUF_OK;
+}
+
+extern "C" shuf_status shuf_shard_continue(shuf_plan_t p, void* ptr, uint64_t m, const uint64_t* d_offsets,
+                                           uint64_t num_segments, uint64_t base, uint32_t first_level, void* scratch,
+                                           uint64_t scratch_bytes, void* stream) {
+    shuf_status s = check_shard_args(p, ptr, d_offsets, scratch, scratch_bytes, m);
+    if (s) return s;
+    if (first_level > kMaxLevels || (m && num_segments == 0)) return SHUF_ERR_INVALID_ARG;
+    if (m <= 1 || num_segments == 0) {
+        p->last_launches = 0;
+        return SHUF_OK;
+    }
+    ShardOpts so;
+    so.n = m;
+    so.base = base;
+    so.first_level = first_level;
+    so.lay = shard_layout(p);
+    return enqueue(p, ptr, d_offsets, num_segments, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1,
+                   nullptr, &so);
 }
 
 extern "C" shuf_status shuf_profile_run(shuf_plan_t p, void* ptr, const uint64_t* d_offsets, uint64_t num_segments,

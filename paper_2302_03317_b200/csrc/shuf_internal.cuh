@@ -114,6 +114,12 @@ struct RunParams {
     unsigned char* items;   // item records: {start, origin, key} + u16 bucket starts [0, k]
     uint32_t* fused;        // with the leaf kernel: the level's children that need the finish kernels
     uint64_t max_fused;     // (k_plan writes them; 0: the finish kernels scan every child)
+    // Sharded problem (NEXT-3, shuf_shard_*): buf0 holds a contiguous slice of one
+    // problem of global positions [seg_base, seg_base + n); its segments are
+    // children at level first_level, keyed K(seed, 0), positions global.
+    uint32_t shard;         // 1: the above; 0: single problem / user segments (D7)
+    uint32_t first_level;   // level of the initial segments (0 unless shard)
+    uint64_t seg_base;      // global position of buf0[0] (shard only)
 };
 
 // Item record of a fused item whose children are all leaves (defer mode):
@@ -220,6 +226,9 @@ __device__ __forceinline__ IpParams ip_resolve(IpParams ip) {
 cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid);
 cudaError_t launch_init_segmented(const RunParams& rp, const LevelParams& lp0, const uint64_t* d_offsets,
                                   uint64_t num_segments, cudaStream_t s, int grid);
+cudaError_t launch_init_shard(const RunParams& rp, const LevelParams& lp0, uint64_t m, uint64_t pos0, cudaStream_t s,
+                              int grid);
+cudaError_t launch_shard_counts(const RunParams& rp, const LevelParams& lp, uint64_t* counts, cudaStream_t s);
 cudaError_t launch_hist(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_scan(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_scatter(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
