@@ -297,8 +297,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="hot", choices=["hot", "c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--mode", default="stable", choices=["stable", "inplace", "sharded"],
+    ap.add_argument("--mode", default="stable", choices=["stable", "inplace", "ipsc", "sharded"],
                     help="inplace: shuf_run_inplace (SURVEY 8(a) a10; aux memory instead of the ping-pong buffer); "
+                         "ipsc: shuf_run_ipsc (NEXT-2, the paper's In-Place ScatterShuffle, D10); "
                          "sharded: ONE problem of N x n elements split over the N ranks (NEXT-3, one level-0 "
                          "all-to-all-v over NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -338,18 +339,22 @@ def main():
         d_off = None
         x = synth.make_input_torch(w, dev)
     plan = shuf.shuf_plan(w.n, w.elem_bytes, w.k, w.L, seed)
-    inplace = args.mode == "inplace"
+    inplace = args.mode in ("inplace", "ipsc")
+    ipsc = args.mode == "ipsc"
     if inplace and d_off is not None:
-        raise SystemExit("--mode inplace: single-shuffle workloads only")
+        raise SystemExit(f"--mode {args.mode}: single-shuffle workloads only")
     if inplace:
-        scratch = torch.empty(max(1, shuf.shuf_aux_bytes_inplace(plan)), dtype=torch.uint8, device=dev)
+        ab = shuf.shuf_aux_bytes_ipsc(plan) if ipsc else shuf.shuf_aux_bytes_inplace(plan)
+        scratch = torch.empty(max(16, ab), dtype=torch.uint8, device=dev)
     else:
         scratch = torch.empty(plan.scratch_bytes if d_off is None else plan.scratch_bytes_segmented(d_off.numel() - 1),
                               dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        if inplace:
+        if ipsc:
+            shuf.shuf_run_ipsc(plan, x, scratch, stream)
+        elif inplace:
             shuf.shuf_run_inplace(plan, x, scratch, stream)
         elif d_off is None:
             shuf.shuf_run(plan, x, scratch, stream)

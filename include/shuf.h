@@ -48,9 +48,11 @@ typedef enum {
     SHUF_ERR_SCRATCH = 4,     /* scratch_bytes smaller than shuf_scratch_bytes() */
     SHUF_ERR_DEPTH = 5,       /* more levels than planned (device-detected)      */
     SHUF_ERR_CUDA = 6,        /* a CUDA runtime error; see shuf_last_cuda_error  */
-    SHUF_ERR_RANK_ORDER = 7   /* device self-check: same-address shared atomics of
+    SHUF_ERR_RANK_ORDER = 7,  /* device self-check: same-address shared atomics of
                                  one warp instruction did not return in lane order
                                  (DESIGN.md 6); rerun with SHUF_RANK_MODE=match   */
+    SHUF_ERR_INTERNAL = 8     /* device self-check of the IpSc mode failed (a
+                                 final bucket size not reached, or R >= 2^32)      */
 } shuf_status;
 
 /* Create a plan for shuffling n elements of elem_bytes bytes each with k
@@ -135,6 +137,28 @@ shuf_status shuf_shard_scatter(shuf_plan_t p, const void *in, uint64_t m, uint64
 shuf_status shuf_shard_continue(shuf_plan_t p, void *ptr, uint64_t m, const uint64_t *d_offsets,
                                 uint64_t num_segments, uint64_t base, uint32_t first_level, void *scratch,
                                 uint64_t scratch_bytes, void *stream);
+
+/* The paper's own In-Place ScatterShuffle (D10
+ * and 6.3; IpSc = RoughScatter P:262-265 in ParRoughScatter's split/merge tree
+ * P:479-491, then FineScatter P:357-425, at every level of Fig. 2).
+ * Shuffles ptr[0..n) IN PLACE with an auxiliary DEVICE buffer `aux` of
+ * shuf_aux_bytes_ipsc() bytes: the staged start of every (ParRoughScatter
+ * node, bucket) of one batch of segments -- O(k * subtasks) words, the paper's
+ * O(k [log_k n + P]) bound (Theorem) with a batch of at most
+ * max(2^21, k * nodes of the root) entries -- plus the levels' segment lists
+ * (16 bytes per segment longer than L).  Deterministic and reproducible: the
+ * result equals the oracle's D10 (oracle_ipsc_shuffle) bit for bit -- a
+ * different permutation from shuf_run's D6 (another algorithm), equally
+ * uniform.  NOT allocation-free on the host side: the level loop plans
+ * batches on the host and SYNCHRONISES the stream once per level.  ptr and
+ * aux 16-byte aligned; elem_bytes 4, 8 or 16 (else SHUF_ERR_UNSUPPORTED).
+ * Device self-check failures return SHUF_ERR_INTERNAL. */
+shuf_status shuf_aux_bytes_ipsc(shuf_plan_t p, uint64_t *bytes);
+shuf_status shuf_run_ipsc(shuf_plan_t p, void *ptr, void *aux, uint64_t aux_bytes, void *stream);
+/* Tests only: IpSc on levels < max_levels (segments of that level left as they
+ * are), Fisher-Yates leaves only if run_leaves -- the oracle's max_levels mode. */
+shuf_status shuf_debug_ipsc_levels(shuf_plan_t p, void *ptr, void *aux, uint64_t aux_bytes, void *stream,
+                                   uint32_t max_levels, int run_leaves);
 
 /* In-place mode (the paper's in-place motivation P:32-36,
  * P:39-43).  Shuffles ptr[0..n) using an auxiliary DEVICE buffer `aux` of

@@ -28,7 +28,8 @@ lib_path = os.environ.get("SHUF_LIB_PATH") or os.path.join(_HERE, "libshuf.so") 
 _lib = None
 
 STATUS = {0: "SHUF_OK", 1: "SHUF_ERR_INVALID_ARG", 2: "SHUF_ERR_UNSUPPORTED", 3: "SHUF_ERR_ALIGNMENT",
-          4: "SHUF_ERR_SCRATCH", 5: "SHUF_ERR_DEPTH", 6: "SHUF_ERR_CUDA", 7: "SHUF_ERR_RANK_ORDER"}
+          4: "SHUF_ERR_SCRATCH", 5: "SHUF_ERR_DEPTH", 6: "SHUF_ERR_CUDA", 7: "SHUF_ERR_RANK_ORDER",
+          8: "SHUF_ERR_INTERNAL"}
 
 # every symbol include/shuf.h declares
 EXPORTED_SYMBOLS = [
@@ -36,7 +37,8 @@ EXPORTED_SYMBOLS = [
     "shuf_debug_bucket_draws", "shuf_debug_fy_draws", "shuf_last_device_error", "shuf_last_cuda_error",
     "shuf_last_launch_count", "shuf_planned_levels", "shuf_destroy", "shuf_status_string", "shuf_profile_run",
     "shuf_last_run_stats", "shuf_rank_mode", "shuf_debug_clocks", "shuf_aux_bytes_inplace", "shuf_run_inplace",
-    "shuf_scratch_bytes_shard", "shuf_shard_scatter", "shuf_shard_continue",
+    "shuf_scratch_bytes_shard", "shuf_shard_scatter", "shuf_shard_continue", "shuf_aux_bytes_ipsc", "shuf_run_ipsc",
+    "shuf_debug_ipsc_levels",
     "shuf_debug_inplace_levels", "shuf_scratch_bytes_segmented", "shuf_sim_rough_scatter",
 ]
 KERNEL_CLASSES = ["init", "hist", "scan", "plan", "scatter", "finish", "leaf"]
@@ -101,6 +103,12 @@ def lib():
         L.shuf_debug_inplace_levels.argtypes = [vp, vp, vp, u64, vp, u32, i32]
         L.shuf_debug_inplace_levels.restype = i32
         L.shuf_rank_mode.restype = i32
+        L.shuf_aux_bytes_ipsc.argtypes = [vp, ctypes.POINTER(u64)]
+        L.shuf_aux_bytes_ipsc.restype = i32
+        L.shuf_run_ipsc.argtypes = [vp, vp, vp, u64, vp]
+        L.shuf_run_ipsc.restype = i32
+        L.shuf_debug_ipsc_levels.argtypes = [vp, vp, vp, u64, vp, u32, i32]
+        L.shuf_debug_ipsc_levels.restype = i32
         L.shuf_scratch_bytes_shard.argtypes = [vp, ctypes.POINTER(u64)]
         L.shuf_scratch_bytes_shard.restype = i32
         L.shuf_shard_scatter.argtypes = [vp, vp, u64, u64, vp, vp, vp, u64, vp]
@@ -249,6 +257,27 @@ def shuf_shard_continue(plan: Plan, x, m: int, d_offsets, base: int, first_level
            "shuf_shard_continue", plan)
 
 
+def shuf_aux_bytes_ipsc(plan: Plan) -> int:
+    v = ctypes.c_uint64(0)
+    _check(lib().shuf_aux_bytes_ipsc(plan.handle, ctypes.byref(v)), "shuf_aux_bytes_ipsc", plan)
+    return int(v.value)
+
+
+def shuf_run_ipsc(plan: Plan, x, aux, stream=None):
+    """The paper's In-Place ScatterShuffle (NEXT-2, D10): in place, deterministic
+    (D10, bit for bit); synchronises the stream once per level."""
+    _check_data(plan, x)
+    _check(lib().shuf_run_ipsc(plan.handle, _dev_ptr(x, "x"), _dev_ptr(aux, "aux"), aux.numel() * aux.element_size(),
+                               _stream(stream)), "shuf_run_ipsc", plan)
+
+
+def shuf_debug_ipsc_levels(plan: Plan, x, aux, max_levels: int, run_leaves: bool, stream=None):
+    _check_data(plan, x)
+    _check(lib().shuf_debug_ipsc_levels(plan.handle, _dev_ptr(x, "x"), _dev_ptr(aux, "aux"),
+                                        aux.numel() * aux.element_size(), _stream(stream), max_levels,
+                                        1 if run_leaves else 0), "shuf_debug_ipsc_levels", plan)
+
+
 def shuf_aux_bytes_inplace(plan: Plan) -> int:
     v = ctypes.c_uint64(0)
     _check(lib().shuf_aux_bytes_inplace(plan.handle, ctypes.byref(v)), "shuf_aux_bytes_inplace", plan)
@@ -367,6 +396,26 @@ def inplace_shuffle(x, k: int, L: int, seed: int, elem_bytes: int | None = None,
     err = shuf_last_device_error(plan, stream)
     if err:
         raise ShufError(err, "shuf_run_inplace (device)")
+    return x
+
+
+def ipsc_shuffle(x, k: int, L: int, seed: int, elem_bytes: int | None = None, aux=None, stream=None,
+                 max_levels: int | None = None, run_leaves: bool = True):
+    """The paper's In-Place ScatterShuffle (NEXT-2, D10) of the rows
+    of x, in place, with O(k * subtasks) words of aux (shuf_aux_bytes_ipsc)."""
+    import torch
+    n = x.shape[0] if x.dim() else 1
+    eb = elem_bytes or (x.numel() * x.element_size() // max(1, n))
+    plan = shuf_plan(n, eb, k, L, seed)
+    if aux is None:
+        aux = torch.empty(max(16, shuf_aux_bytes_ipsc(plan)), dtype=torch.uint8, device=x.device)
+    if max_levels is None:
+        shuf_run_ipsc(plan, x, aux, stream)
+    else:
+        shuf_debug_ipsc_levels(plan, x, aux, max_levels, run_leaves, stream)
+    err = shuf_last_device_error(plan, stream)
+    if err:
+        raise ShufError(err, "shuf_run_ipsc (device)")
     return x
 
 

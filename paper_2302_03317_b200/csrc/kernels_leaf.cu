@@ -203,6 +203,27 @@ struct IpChildLeaves {
     }
 };
 
+// Leaf `lane` of unit u of an IpSc batch (kernels_ipsc.cu): children
+// 32g .. 32g+31 of batch segment s, final bucket starts S[s * (k+1) + b].
+struct IpscLeaves {
+    const uint64_t* S;
+    uint32_t nseg, k, groups;
+    uint64_t seed;
+    __device__ __forceinline__ uint64_t units() const { return (uint64_t)nseg * groups; }
+    __device__ __forceinline__ Leaf get(uint64_t u, uint32_t lane) const {
+        Leaf f{0, 0, 0, 0};
+        const uint32_t s = (uint32_t)(u / groups), b = (uint32_t)(u % groups) * 32u + lane;
+        if (b < k) {
+            const uint64_t* T = S + (uint64_t)s * (k + 1) + b;
+            f.start = T[0];
+            f.len = T[1] - T[0];
+            f.origin = 0;
+            f.key = seed;  // K(seed, 0) (D2); positions are problem-relative
+        }
+        return f;
+    }
+};
+
 template <int EB, class Src>
 __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned char* src, const Src& ls,
                                            uint32_t slot_bytes) {
@@ -357,8 +378,15 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_ipchildren(RunParams rp, 
     run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
 }
 
-// mode: 0 children, 1 segments, 2 items, 3 in-place children
+template <int EB>
+__global__ void __launch_bounds__(kLeafThreads) k_leaf_ipsc(RunParams rp, const uint64_t* __restrict__ S, uint32_t nseg) {
+    const IpscLeaves ls{S, nseg, rp.k, (rp.k + 31) / 32, rp.seed};
+    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
+}
+
+// mode: 0 children, 1 segments, 2 items, 3 in-place children, 4 IpSc children
 static void* leaf_fn(uint32_t eb, int mode) {
+    if (mode == 4) return eb == 4 ? (void*)k_leaf_ipsc<4> : eb == 8 ? (void*)k_leaf_ipsc<8> : (void*)k_leaf_ipsc<16>;
     if (mode == 3) return eb == 4 ? (void*)k_leaf_ipchildren<4> : eb == 8 ? (void*)k_leaf_ipchildren<8>
                                                                         : (void*)k_leaf_ipchildren<16>;
     switch (eb) {
@@ -371,7 +399,7 @@ static void* leaf_fn(uint32_t eb, int mode) {
 
 cudaError_t configure_leaf(uint32_t eb, uint32_t L) {
     (void)L;  // the attribute is the limit: plans of other sizes share the kernels
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
         cudaError_t e = cudaFuncSetAttribute(leaf_fn(eb, mode), cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
         if (e) return e;
     }
@@ -400,6 +428,12 @@ cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets,
 cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp};
     return cudaLaunchKernel(leaf_fn(rp.eb, 2), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L), s);
+}
+
+cudaError_t launch_leaf_ipsc(const RunParams& rp, const uint64_t* S, uint32_t nseg, cudaStream_t s, int grid) {
+    if (nseg == 0) return cudaSuccess;
+    void* args[] = {(void*)&rp, (void*)&S, (void*)&nseg};
+    return cudaLaunchKernel(leaf_fn(rp.eb, 4), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L), s);
 }
 
 cudaError_t launch_leaf_ipchildren(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid) {

@@ -719,6 +719,239 @@ extern "C" shuf_status shuf_run(shuf_plan_t p, void* ptr, void* scratch, uint64_
     return enqueue(p, ptr, nullptr, 0, scratch, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
 }
 
+// ---------------------------------------------------------------- IpSc ---
+// NEXT-2 (kernels_ipsc.cu): the paper's In-Place ScatterShuffle, level by
+// level; the host plans batches of segments whose ParRoughScatter trees fit
+// the node table, and reads each level's segment list back (one sync/level).
+struct IpscLayout {
+    uint64_t header, root, segs[2], cnt, bsegs, work, stab, S, total;
+    uint64_t max_segs, max_bseg, E;
+};
+
+static uint32_t ipsc_depth_host(uint64_t m, uint32_t k) {
+    const uint64_t n0 = (uint64_t)k * k;
+    uint32_t t = 0;
+    while (t < 11u && (m >> (t + 1)) >= n0) ++t;
+    return t;
+}
+
+static IpscLayout ipsc_layout(const shuf_plan_s* p) {
+    IpscLayout l{};
+    const uint64_t n = p->n, k = p->k;
+    l.max_segs = n / ((uint64_t)p->L + 1) + 1;
+    const uint64_t root_entries = ((2ull << ipsc_depth_host(n, p->k)) - 1) * k;
+    uint64_t E = l.max_segs * k;
+    if (E > (1ull << 21)) E = 1ull << 21;
+    if (E < root_entries) E = root_entries;
+    l.E = E;
+    l.max_bseg = E / k;
+    uint64_t off = 0;
+    auto take = [&off](uint64_t bytes) {
+        const uint64_t at = off;
+        off = align_up(off + bytes, 256);
+        return at;
+    };
+    l.header = take(sizeof(Header));
+    l.root = take(16);
+    l.segs[0] = take(l.max_segs * 16);
+    l.segs[1] = take(l.max_segs * 16);
+    l.cnt = take(8);
+    l.bsegs = take(l.max_bseg * sizeof(IpscSeg));
+    l.work = take(l.max_bseg * 8);
+    l.stab = take(E * 8);
+    l.S = take(l.max_bseg * (k + 1) * 8);
+    l.total = off;
+    return l;
+}
+
+extern "C" shuf_status shuf_aux_bytes_ipsc(shuf_plan_t p, uint64_t* bytes) {
+    if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) return SHUF_ERR_UNSUPPORTED;
+    *bytes = ipsc_layout(p).total;
+    return SHUF_OK;
+}
+
+static shuf_status enqueue_ipsc(shuf_plan_s* p, void* ptr, void* aux, cudaStream_t st, uint32_t max_levels,
+                                int run_leaves) {
+    p->last_launches = 0;
+    cudaError_t e = device_setup(p);
+    if (e) return cuda_fail(p, e);
+    if (leaf_smem_bytes(p->eb, p->L) > kSmemLimit) return SHUF_ERR_UNSUPPORTED;
+    if (!p->leafk) {
+        if ((e = configure_leaf(p->eb, p->L))) return cuda_fail(p, e);
+        int ol = 1;
+        if ((e = occupancy_leaf(p->eb, p->L, &ol))) return cuda_fail(p, e);
+        p->grid_leaf = p->sms * (ol < 1 ? 1 : ol);
+    }
+    const IpscLayout l = ipsc_layout(p);
+    unsigned char* ax = static_cast<unsigned char*>(aux);
+    Header* hdr = reinterpret_cast<Header*>(ax + l.header);
+    p->last_hdr = hdr;
+    RunParams rp{};
+    rp.buf0 = static_cast<unsigned char*>(ptr);
+    rp.hdr = hdr;
+    rp.n = p->n;
+    rp.eb = p->eb;
+    rp.k = p->k;
+    rp.L = p->L;
+    rp.S_fuse = p->S_fuse;
+    rp.chunk = p->chunk;
+    rp.max_levels = max_levels;
+    rp.planned_levels = kMaxLevels;
+    rp.run_leaves = run_leaves;
+    rp.bp = make_bucket_params(p->k);
+    rp.seed = p->seed;
+    uint64_t launches = 0;
+    Prof* prof = nullptr;
+    if ((e = cudaMemsetAsync(hdr, 0, sizeof(Header), st))) return cuda_fail(p, e);
+    const uint64_t n = p->n, k = p->k;
+    if (n <= p->L) {  // the whole array is one leaf (Fig. 2)
+        if (run_leaves && n >= 2) {
+            const uint64_t root[2] = {0, n};
+            uint64_t* d_root = reinterpret_cast<uint64_t*>(ax + l.root);
+            if ((e = cudaMemcpyAsync(d_root, root, sizeof root, cudaMemcpyHostToDevice, st))) return cuda_fail(p, e);
+            LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, d_root, 1, st, 1));
+        }
+        p->last_launches = launches;
+        return SHUF_OK;
+    }
+    IpscParams P{};
+    P.X = static_cast<unsigned char*>(ptr);
+    P.k = p->k;
+    P.L = p->L;
+    P.seed = p->seed;
+    P.segs = reinterpret_cast<const IpscSeg*>(ax + l.bsegs);
+    P.s_tab = reinterpret_cast<uint64_t*>(ax + l.stab);
+    P.S = reinterpret_cast<uint64_t*>(ax + l.S);
+    P.next_cnt = reinterpret_cast<uint32_t*>(ax + l.cnt);
+    P.max_next = l.max_segs;
+    P.hdr = hdr;
+    P.run_leaves = (uint32_t)run_leaves;
+    uint32_t rs_grid = 2u * (uint32_t)p->sms;  // SHUF_IPSC_RSGRID=<CTAs per SM> (experiments)
+    if (const char* g = std::getenv("SHUF_IPSC_RSGRID")) rs_grid = (uint32_t)std::atoi(g) * (uint32_t)p->sms;
+    uint32_t tsmall = 0;  // (the capacity's tree depth; launches size their own)
+    const uint32_t cap = std::getenv("SHUF_IPSC_NOSMALL") ? 0u : ipsc_small_cap(p->k, p->eb, &tsmall);
+    IpscSeg* d_bsegs = reinterpret_cast<IpscSeg*>(ax + l.bsegs);
+    uint2* d_work = reinterpret_cast<uint2*>(ax + l.work);
+    std::vector<uint64_t> cur = {0, n}, nxt;
+    std::vector<IpscSeg> bs;
+    std::vector<uint2> work;
+    std::vector<uint32_t> wofs;
+    {
+        uint64_t* l0 = reinterpret_cast<uint64_t*>(ax + l.segs[0]);
+        if ((e = cudaMemcpyAsync(l0, cur.data(), 16, cudaMemcpyHostToDevice, st))) return cuda_fail(p, e);
+    }
+    for (uint32_t lv = 0; !cur.empty() && lv < max_levels; ++lv) {
+        if (lv > 255) return SHUF_ERR_DEPTH;
+        const int slot = (lv + 1) & 1;
+        P.level = lv;
+        P.next = reinterpret_cast<uint64_t*>(ax + l.segs[slot]);
+        if ((e = cudaMemsetAsync(P.next_cnt, 0, 4, st))) return cuda_fail(p, e);
+        const size_t nseg = cur.size() / 2;
+        // segments of at most `cap` elements: one fused shared-memory launch over the level's list
+        // (shared memory sized for the longest of them: more CTAs per SM when they are short)
+        size_t nsmall = 0;
+        uint64_t mmax = 0;
+        for (size_t q = 0; q < nseg; ++q)
+            if (cur[2 * q + 1] <= cap) {
+                ++nsmall;
+                if (cur[2 * q + 1] > mmax) mmax = cur[2 * q + 1];
+            }
+        if (nsmall) {
+            uint32_t tl = 0;
+            while (tl < 11u && (mmax >> (tl + 1)) >= k * k) ++tl;
+            LAUNCH(SHUF_K_FINISH, launch_ipsc_small(P, p->eb, reinterpret_cast<const uint64_t*>(ax + l.segs[lv & 1]),
+                                                    (uint32_t)nseg, (uint32_t)((mmax + 15) & ~15ull), tl, st,
+                                                    4 * p->sms));
+        }
+        for (size_t s0 = 0; s0 < nseg;) {
+            // batch: segments while their node tables fit E entries
+            bs.clear();
+            uint64_t entries = 0;
+            uint32_t tmax = 0;
+            size_t s1 = s0;
+            for (; s1 < nseg; ++s1) {
+                IpscSeg g{};
+                g.a = cur[2 * s1];
+                g.m = cur[2 * s1 + 1];
+                if (g.m <= cap) continue;  // the shared-memory kernel's
+                g.t = ipsc_depth_host(g.m, p->k);
+                const uint64_t nodes = (2ull << g.t) - 1;
+                if (!bs.empty() && (entries + nodes * k > l.E || bs.size() >= l.max_bseg)) break;
+                g.node_base = entries / k;
+                entries += nodes * k;
+                if (g.t > tmax) tmax = g.t;
+                bs.push_back(g);
+            }
+            // work lists: leaf subtasks, then the inner nodes depth by depth (deepest first)
+            work.clear();
+            wofs.clear();
+            for (int d = (int)tmax; d >= 0; --d) {
+                wofs.push_back((uint32_t)work.size());
+                for (uint32_t si = 0; si < bs.size(); ++si) {
+                    const uint32_t t = bs[si].t;
+                    if (d == (int)tmax) {  // first launch: every segment's leaves
+                        for (uint32_t v = 1u << t; v < (2u << t); ++v) work.push_back(make_uint2(si, v));
+                    } else if ((uint32_t)d < t) {
+                        for (uint32_t v = 1u << d; v < (2u << d); ++v) work.push_back(make_uint2(si, v));
+                    }
+                }
+            }
+            wofs.push_back((uint32_t)work.size());
+            s0 = s1;
+            if (bs.empty()) continue;
+            if (work.size() > l.max_bseg) return SHUF_ERR_SCRATCH;  // (nodes <= E / k = max_bseg)
+            if ((e = cudaMemcpyAsync(d_bsegs, bs.data(), bs.size() * sizeof(IpscSeg), cudaMemcpyHostToDevice, st)))
+                return cuda_fail(p, e);
+            if ((e = cudaMemcpyAsync(d_work, work.data(), work.size() * sizeof(uint2), cudaMemcpyHostToDevice, st)))
+                return cuda_fail(p, e);
+            for (size_t q = 0; q + 1 < wofs.size(); ++q) {
+                const uint32_t nw = wofs[q + 1] - wofs[q];
+                P.work = d_work + wofs[q];
+                const bool wide = nw < (uint32_t)p->sms;
+                LAUNCH(SHUF_K_SCATTER, launch_ipsc_rs(P, p->eb, nw, q > 0, wide, rs_grid, st));
+            }
+            LAUNCH(SHUF_K_FINISH, launch_ipsc_fine(P, p->eb, (uint32_t)bs.size(), st));
+            LAUNCH(SHUF_K_PLAN, launch_ipsc_children(P, (uint32_t)bs.size(), st, p->grid_small));
+            if (run_leaves) LAUNCH(SHUF_K_LEAF, launch_leaf_ipsc(rp, P.S, (uint32_t)bs.size(), st, p->grid_leaf));
+        }
+        uint32_t cnt = 0, err = 0;
+        if ((e = cudaMemcpyAsync(&cnt, P.next_cnt, 4, cudaMemcpyDeviceToHost, st))) return cuda_fail(p, e);
+        if ((e = cudaMemcpyAsync(&err, &hdr->error, 4, cudaMemcpyDeviceToHost, st))) return cuda_fail(p, e);
+        if ((e = cudaStreamSynchronize(st))) return cuda_fail(p, e);
+        if (err) break;  // reported by shuf_last_device_error
+        nxt.resize(2 * (size_t)cnt);
+        if (cnt && (e = cudaMemcpy(nxt.data(), P.next, nxt.size() * 8, cudaMemcpyDeviceToHost))) return cuda_fail(p, e);
+        cur.swap(nxt);
+    }
+    p->last_launches = launches;
+    return SHUF_OK;
+}
+
+static shuf_status check_ipsc_args(shuf_plan_s* p, void* ptr, void* aux, uint64_t aux_bytes) {
+    if (!p) return SHUF_ERR_INVALID_ARG;
+    if (p->idx) return SHUF_ERR_UNSUPPORTED;
+    if (p->n > 1 && (!ptr || !aux)) return SHUF_ERR_INVALID_ARG;
+    if (((uintptr_t)ptr & 15u) || ((uintptr_t)aux & 15u)) return SHUF_ERR_ALIGNMENT;
+    if (p->n > 1 && aux_bytes < ipsc_layout(p).total) return SHUF_ERR_SCRATCH;
+    return SHUF_OK;
+}
+
+extern "C" shuf_status shuf_run_ipsc(shuf_plan_t p, void* ptr, void* aux, uint64_t aux_bytes, void* stream) {
+    shuf_status s = check_ipsc_args(p, ptr, aux, aux_bytes);
+    if (s) return s;
+    if (p->n <= 1) return SHUF_OK;
+    return enqueue_ipsc(p, ptr, aux, static_cast<cudaStream_t>(stream), 0xFFFFFFFFu, 1);
+}
+
+extern "C" shuf_status shuf_debug_ipsc_levels(shuf_plan_t p, void* ptr, void* aux, uint64_t aux_bytes, void* stream,
+                                              uint32_t max_levels, int run_leaves) {
+    shuf_status s = check_ipsc_args(p, ptr, aux, aux_bytes);
+    if (s) return s;
+    if (p->n <= 1) return SHUF_OK;
+    return enqueue_ipsc(p, ptr, aux, static_cast<cudaStream_t>(stream), max_levels, run_leaves ? 1 : 0);
+}
+
 // ------------------------------------------------------------ in-place ---
 extern "C" shuf_status shuf_aux_bytes_inplace(shuf_plan_t p, uint64_t* bytes) {
     if (!p || !bytes) return SHUF_ERR_INVALID_ARG;
@@ -1154,6 +1387,7 @@ extern "C" const char* shuf_status_string(shuf_status s) {
     case SHUF_ERR_DEPTH: return "more scatter levels than planned";
     case SHUF_ERR_CUDA: return "CUDA error";
     case SHUF_ERR_RANK_ORDER: return "ordered-atomic ranking self-check failed (use SHUF_RANK_MODE=match)";
+    case SHUF_ERR_INTERNAL: return "IpSc device self-check failed";
     }
     return "unknown status";
 }

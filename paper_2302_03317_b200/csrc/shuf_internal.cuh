@@ -222,7 +222,38 @@ __device__ __forceinline__ IpParams ip_resolve(IpParams ip) {
 }
 #endif
 
+// In-place ScatterShuffle of the paper (NEXT-2, kernels_ipsc.cu): one batch
+// of segments of a level; heap node v of segment s has node slot
+// segs[s].node_base + v - 1 in the s-table (k staged starts per slot).
+struct IpscSeg {
+    uint64_t a, m;       // [a, a+m) at the batch's level
+    uint64_t node_base;  // first node slot
+    uint32_t t, pad;     // ParRoughScatter depth
+};
+
+struct IpscParams {
+    unsigned char* X;
+    uint32_t k, L, level, run_leaves;
+    uint64_t seed;
+    const IpscSeg* segs;
+    const uint2* work;   // (segment, heap node) per CTA of an RoughScatter launch
+    uint64_t* s_tab;     // node slot * k + i
+    uint64_t* S;         // final bucket starts, segment * (k + 1) + i
+    uint64_t* next;      // next level's (start, len) list
+    uint32_t* next_cnt;
+    uint64_t max_next;
+    Header* hdr;
+};
+
 // ------------------------------------------------------ host launchers ---
+cudaError_t launch_ipsc_rs(const IpscParams& P, uint32_t eb, uint32_t nwork, bool merge, bool wide, uint32_t grid,
+                           cudaStream_t s);
+cudaError_t launch_ipsc_fine(const IpscParams& P, uint32_t eb, uint32_t nseg, cudaStream_t s);
+cudaError_t launch_ipsc_children(const IpscParams& P, uint32_t nseg, cudaStream_t s, int grid);
+uint32_t ipsc_small_cap(uint32_t k, uint32_t eb, uint32_t* tmax);
+cudaError_t launch_ipsc_small(const IpscParams& P, uint32_t eb, const uint64_t* list, uint32_t count, uint32_t cap,
+                              uint32_t tmax, cudaStream_t s, int grid);
+cudaError_t launch_leaf_ipsc(const RunParams& rp, const uint64_t* S, uint32_t nseg, cudaStream_t s, int grid);
 cudaError_t launch_init(const RunParams& rp, const LevelParams& lp0, cudaStream_t s, int grid);
 cudaError_t launch_init_segmented(const RunParams& rp, const LevelParams& lp0, const uint64_t* d_offsets,
                                   uint64_t num_segments, cudaStream_t s, int grid);
