@@ -10,6 +10,7 @@ digests the GPU output the same way, so equal digest lists mean equal arrays
 Jobs (BASELINE.json configs at full size):
 - ``hot``: 2^30 u32 iota, k=256, L=4096, seed=1 (the metric's run);
 - ``c3``:  1,000,000,007 SplitMix64(3) u64 values, k=256, L=2048, seed=3;
+- ``hot_ipsc``: HOT through the paper's In-Place ScatterShuffle (D10, NEXT-2);
 - ``c4pi``: the permutation pi of config 4 (2^32 elements, k=1024, L=2048,
   seed=11) computed on u32 iota -- pi does not depend on the element size
   (D6), so the GPU's 16-byte records must carry key[j] = pi(j)
@@ -43,6 +44,9 @@ def job(name: str, n: int | None = None) -> list:
     if name == "c4pi":
         w = synth.WORKLOADS["c4"]
         a = np.arange(w.n if n is None else n, dtype=np.uint32)
+    elif name == "hot_ipsc":
+        w = synth.WORKLOADS["hot"]
+        return digests(oracle.ipsc_shuffle(synth.make_input_np(w, n=n), w.k, w.L, w.seed))
     else:
         w = synth.WORKLOADS[name]
         a = synth.make_input_np(w, n=n)

@@ -77,8 +77,8 @@ def oracle_jobs():
     from concurrent.futures import ProcessPoolExecutor
 
     from tests import oracle_digest
-    ex = ProcessPoolExecutor(max_workers=3, mp_context=multiprocessing.get_context("spawn"))
-    futs = {name: ex.submit(oracle_digest.job, name) for name in ("c4pi", "c3", "hot")}
+    ex = ProcessPoolExecutor(max_workers=4, mp_context=multiprocessing.get_context("spawn"))
+    futs = {name: ex.submit(oracle_digest.job, name) for name in ("c4pi", "c3", "hot", "hot_ipsc")}
     yield futs
     procs = list((ex._processes or {}).values())
     ex.shutdown(wait=False, cancel_futures=True)
@@ -109,6 +109,36 @@ def test_hot_full_bit_exact(oracle_jobs):
     got = _gpu_digests(x.view(torch.int32))
     del x
     _assert_same(got, oracle_jobs["hot"].result(), "hot")
+
+
+def test_hot_sharded_two_ranks_full_bit_exact(oracle_jobs):
+    """NEXT-3 at the metric's size: HOT as ONE problem split over two ranks
+    (run one after another on this GPU, sharded.simulate_sharded: level-0
+    scatter of each slice at its global positions, the exchange layout's
+    piece moves, D6 from level 1 on each owner's buckets); the concatenated
+    output must equal the single-problem oracle run."""
+    from paper_2302_03317_b200 import sharded
+    w = synth.WORKLOADS["hot"]
+    x = synth.make_input_torch(w, DEV)
+    out, parts = sharded.simulate_sharded(x, w.n, 2, w.k, w.L, w.seed, elem_bytes=4)
+    del x
+    assert parts[0][0] == 0 and parts[0][1] + parts[1][1] == w.n
+    got = _gpu_digests(out.view(torch.int32))
+    del out
+    _assert_same(got, oracle_jobs["hot"].result(), "hot sharded x2")
+
+
+def test_hot_ipsc_full_bit_exact(oracle_jobs):
+    """NEXT-2 at the metric's size: HOT through the paper's In-Place
+    ScatterShuffle (shuf_run_ipsc: ParRoughScatter's 2^11 subtasks at the
+    root, FineScatter, the small-segment kernel at level 2, leaves), whole
+    array against the oracle's D10."""
+    w = synth.WORKLOADS["hot"]
+    x = synth.make_input_torch(w, DEV)
+    shuf.ipsc_shuffle(x, w.k, w.L, w.seed, elem_bytes=4)
+    got = _gpu_digests(x.view(torch.int32))
+    del x
+    _assert_same(got, oracle_jobs["hot_ipsc"].result(), "hot ipsc")
 
 
 def test_c3_full_bit_exact(oracle_jobs):
