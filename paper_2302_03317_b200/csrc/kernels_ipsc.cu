@@ -80,6 +80,33 @@ __device__ __forceinline__ void node_range(uint64_t a, uint64_t m, uint32_t k, u
 
 __device__ __forceinline__ void ipsc_latch(Header* h, uint32_t code) { atomicCAS(&h->error, 0u, code); }
 
+// Swap X[p + x] <-> X[q - x] for x in [0, n) (MIRROR), or X[p + x] <-> X[p + x + q]
+// (stride q >= n), by threads gt = 0.. of a group of G.  The pairs are
+// disjoint, so each thread keeps four in flight (memory-level parallelism).
+template <typename E, bool MIRROR>
+__device__ __forceinline__ void pair_swaps(E* X, uint64_t p, uint64_t q, uint64_t n, uint32_t gt, uint32_t G) {
+    auto other = [&](uint64_t x) { return MIRROR ? q - x : p + x + q; };
+    uint64_t x = gt;
+    for (; x + 3ull * G < n; x += 4ull * G) {
+        E a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = X[p + x + u * (uint64_t)G];
+            b[u] = X[other(x + u * (uint64_t)G)];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            X[p + x + u * (uint64_t)G] = b[u];
+            X[other(x + u * (uint64_t)G)] = a[u];
+        }
+    }
+    for (; x < n; x += G) {
+        const E t0 = X[p + x];
+        X[p + x] = X[other(x)];
+        X[other(x)] = t0;
+    }
+}
+
 
 // ---------------------------------------------------------- RoughScatter --
 // Shared scratch of one RoughScatter run by NT threads taking U steps each
@@ -133,11 +160,7 @@ __device__ void rs_node(typename ElemT<EB>::type* X, const IpscParams& P, uint64
             node_range(a, m, k, i, v, lo, hi);
             const uint64_t mid = lo + (hi - lo) / 2, s1 = sl[i], s2 = sr[i];
             const uint64_t A = mid - s1, B = s2 - mid, mn = A < B ? A : B;
-            for (uint64_t x = tid; x < mn; x += NT) {
-                const E t0 = X[s1 + x];
-                X[s1 + x] = X[s2 - 1 - x];
-                X[s2 - 1 - x] = t0;
-            }
+            pair_swaps<E, true>(X, s1, s2 - 1, mn, tid, NT);
         }
     }
     __syncthreads();
@@ -232,14 +255,14 @@ __device__ void rs_node_warp(typename ElemT<EB>::type* X, const IpscParams& P, u
         c[i] = 0;
         cap[i] = (uint32_t)(hi - st);
         full |= hi == st;
-        if (MERGE) {  // staged items of the first half <-> placed items of the second half
+    }
+    if (MERGE) {  // staged items of the first half <-> placed items of the second half, bucket by bucket
+        for (uint32_t i = 0; i < k; ++i) {
+            uint64_t lo, hi;
+            node_range(a, m, k, i, v, lo, hi);
             const uint64_t mid = lo + (hi - lo) / 2, s1 = sl[i], s2 = sr[i];
             const uint64_t A = mid - s1, B = s2 - mid, mn = A < B ? A : B;
-            for (uint64_t x = 0; x < mn; ++x) {
-                const E t0 = X[s1 + x];
-                X[s1 + x] = X[s2 - 1 - x];
-                X[s2 - 1 - x] = t0;
-            }
+            pair_swaps<E, true>(X, s1, s2 - 1, mn, lane, 32u);
         }
     }
     __syncwarp();
@@ -419,9 +442,14 @@ struct FineScratch {
 template <typename E, bool DOWN>
 __device__ __forceinline__ void sweep_move(E* X, uint64_t c, uint64_t x, uint64_t Pp, uint32_t gt, uint32_t G) {
     if (Pp == 0) return;
-    const uint64_t nr = Pp < x ? Pp : x;
+    if (x <= Pp) {  // every class holds two elements: x disjoint swaps at distance P
+        pair_swaps<E, false>(X, DOWN ? c - x : c, Pp, x, gt, G);
+        return;
+    }
+    const uint64_t nr = Pp < x ? Pp : x;  // here x > P: chains of C + 1 >= 3 elements
+    const bool n32 = ((x | Pp) >> 32) == 0;
     for (uint64_t r = gt; r < nr; r += G) {
-        const uint64_t C = (x - 1 - r) / Pp + 1;
+        const uint64_t C = (n32 ? (uint64_t)((uint32_t)(x - 1 - r) / (uint32_t)Pp) : (x - 1 - r) / Pp) + 1;
         if (DOWN) {  // unit u swaps (c-1-u, c-1-u+P): each class's top element drops to its bottom
             const uint64_t q0 = c - x + r;
             const E top = X[q0 + C * Pp];
@@ -461,7 +489,9 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
         cnt[i] = 0;
         myR += hi - s[i];
     }
-    atomicAdd(s_R, myR);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) myR += __shfl_xor_sync(0xFFFFFFFFu, myR, o);
+    if ((tid & 31u) == 0 && myR) atomicAdd(s_R, myR);
     for (uint32_t x = tid; x < H; x += NT) {
         hkey[x] = 0;
         hval[x] = 0;
@@ -485,42 +515,40 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
         }
     }
     __syncthreads();
-    // TwoSweep.  Boundary i's move touches [c - x, c + P) (sweep 1)
-    // or [c, c + P + x) (sweep 2) with c = b_{i+1}, P = s_{i+1} - b_{i+1}; its
-    // parameters do not depend on the other boundaries' moves of the same sweep,
-    // only its data does (the sweep order), so a group barrier after each move.
+    const bool tk = P.clk && blockIdx.x == 0 && tid == 0 && *s_R == R && WARP_SWEEP;
+    if (tk && P.clk[2] == 0) P.clk[2] = clock64();
+    // TwoSweep.  Boundary i makes ONE move: sweep 1 (ascending) when
+    // D_i < 0, sweep 2 (descending) when D_i > 0, at c = b_{i+1}, with stride
+    // P = s_{i+1} - b_{i+1} -- values of the state before the sweeps, since only
+    // the boundary's own move changes them; afterwards b_{i+1} = s_{i+1} - P =
+    // b_{i+1} + D_i and e_i = b_{i+1}.  The data order between the moves is
+    // kept by a group barrier after each.
     if (!WARP_SWEEP || tid < 32) {
         const uint32_t G = WARP_SWEEP ? 32u : NT, gt = tid;
-        for (uint32_t i = 0; i + 1 < k; ++i) {  // sweep 1 ascending: -D_i slots of B_i's end -> B_{i+1}
+        for (uint32_t i = 0; i + 1 < k; ++i) {  // sweep 1: -D_i slots of B_i's end -> B_{i+1}
             const int64_t xd = -Dp[i];
             if (xd <= 0) continue;
-            const uint64_t x = (uint64_t)xd, c = b[i + 1], Pp = s[i + 1] - c;
-            sweep_move<E, true>(X, c, x, Pp, gt, G);
+            sweep_move<E, true>(X, b[i + 1], (uint64_t)xd, s[i + 1] - b[i + 1], gt, G);
             if (WARP_SWEEP) __syncwarp();
             else __syncthreads();
-            if (gt == 0) {
-                e[i] -= x;
-                b[i + 1] -= x;
-                s[i + 1] -= x;
-            }
         }
-        if (WARP_SWEEP) __syncwarp();
-        else __syncthreads();
-        for (uint32_t i = k - 1; i-- > 0;) {  // sweep 2 descending: D_i slots of B_{i+1}'s start -> B_i
+        for (uint32_t i = k - 1; i-- > 0;) {  // sweep 2: D_i slots of B_{i+1}'s start -> B_i
             const int64_t xd = Dp[i];
             if (xd <= 0) continue;
-            const uint64_t x = (uint64_t)xd, c = b[i + 1], Pp = s[i + 1] - c;
-            sweep_move<E, false>(X, c, x, Pp, gt, G);
+            sweep_move<E, false>(X, b[i + 1], (uint64_t)xd, s[i + 1] - b[i + 1], gt, G);
             if (WARP_SWEEP) __syncwarp();
             else __syncthreads();
-            if (gt == 0) {
-                b[i + 1] += x;
-                s[i + 1] += x;
-                e[i] += x;
-            }
         }
     }
     __syncthreads();
+    for (uint32_t i = tid; i + 1 < k; i += NT) {
+        b[i + 1] += (uint64_t)Dp[i];
+        s[i + 1] += (uint64_t)Dp[i];
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i + 1 < k; i += NT) e[i] = b[i + 1];
+    __syncthreads();
+    if (tk && P.clk[3] == 0) P.clk[3] = clock64();
     if (tid == 0) {
         uint64_t t = 0;
         for (uint32_t i = 0; i < k; ++i) {
@@ -534,34 +562,49 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
     __syncthreads();
     // stash shuffle: Fisher-Yates on V[t] = X[p_t], rounds of conflict-free prefixes
     uint64_t top = R ? R - 1 : 0;
-    if (WARP_SWEEP) {  // warp 0, rounds of <= 32 steps; conflicts found by match_any and shuffles
+    if (WARP_SWEEP) {  // warp 0, rounds of <= 32 steps; conflicts found by match_any and an OR-reduction
+        // positions p_t - a as u16 in the (here unused) hash region when they fit
+        uint16_t* posT = reinterpret_cast<uint16_t*>(hkey);
+        const bool tab = R <= 8u * H && m <= 65536u;
+        if (tab)
+            for (uint32_t t = tid; t < (uint32_t)R; t += NT) posT[t] = (uint16_t)(staged_pos(cum, s, k, t) - a);
+        __syncthreads();
         if (tid < 32) {
             const uint32_t lane = tid, lt = (1u << lane) - 1u;
-            while (top >= 1) {
-                const bool valid = top >= (uint64_t)lane + 1;
-                const uint32_t i = valid ? (uint32_t)(top - lane) : 0u;
-                const uint32_t j = valid ? ipsc_draw(key, TAG_IPSC_FY, i, 0u, P.level, a, i + 1) : 0u;
+            uint32_t tp = (uint32_t)top;
+            uint32_t jn = tp >= lane + 1 ? ipsc_draw(key, TAG_IPSC_FY, tp - lane, 0u, P.level, a, tp - lane + 1) : 0u;
+            while (tp >= 1) {
+                const bool valid = tp >= lane + 1;
+                const uint32_t i = valid ? tp - lane : 0u;
+                const uint32_t j = valid ? jn : 0u;
+                // the draws of the next 32 steps, assuming this round runs all 32 (the usual case)
+                const uint32_t tq = tp >= 32u ? tp - 32u : 0u;
+                const uint32_t jspec = tq >= lane + 1 ? ipsc_draw(key, TAG_IPSC_FY, tq - lane, 0u, P.level, a, tq - lane + 1) : 0u;
                 const unsigned long long mk = valid ? (unsigned long long)j : (1ull << 32) | lane;
                 bool conflict = (__match_any_sync(0xFFFFFFFFu, mk) & lt) != 0;  // an earlier step shares my partner
-                for (uint32_t q = 0; q < 31; ++q) {  // an earlier step's partner is my own index
-                    const uint32_t jq = __shfl_sync(0xFFFFFFFFu, j, q);
-                    conflict |= (q < lane && jq == i);
-                }
+                // an earlier step's partner is my own index: lane l' with j = tp - l (l > l') hits lane l
+                const uint32_t d = tp - j;
+                const uint32_t hit = __reduce_or_sync(0xFFFFFFFFu, valid && d < 32u && d > lane ? 1u << d : 0u);
+                conflict |= (hit >> lane) & 1u;
                 const uint32_t cm = __ballot_sync(0xFFFFFFFFu, valid && conflict);
                 const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, valid));
                 const uint32_t pre = cm ? (uint32_t)(__ffs(cm) - 1) : nv;
                 if (valid && lane < pre && i != j) {
-                    const uint64_t pi = staged_pos(cum, s, k, i), pj = staged_pos(cum, s, k, j);
+                    const uint64_t pi = tab ? a + posT[i] : staged_pos(cum, s, k, i);
+                    const uint64_t pj = tab ? a + posT[j] : staged_pos(cum, s, k, j);
                     const E t0 = X[pi];
                     X[pi] = X[pj];
                     X[pj] = t0;
                 }
                 __syncwarp();
-                top -= pre;
+                tp -= pre;
+                if (pre == 32u) jn = jspec;
+                else if (tp >= lane + 1) jn = ipsc_draw(key, TAG_IPSC_FY, tp - lane, 0u, P.level, a, tp - lane + 1);
             }
         }
         top = 0;
         __syncthreads();
+        if (tk && P.clk[4] == 0) P.clk[4] = clock64();
     }
     for (uint64_t stamp = 1; top >= 1; ++stamp) {
         const uint64_t o = tid;
@@ -669,6 +712,8 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_ipsc_small(IpscParams P, c
     for (uint32_t si = blockIdx.x; si < count; si += gridDim.x) {
         const uint64_t a = list[2 * (uint64_t)si], m = list[2 * (uint64_t)si + 1];
         if (m > cap) continue;  // the HBM kernels' segment
+        const bool tk = P.clk && blockIdx.x == 0 && tid == 0 && si == 0;
+        if (tk) P.clk[0] = clock64();
         for (uint64_t x = tid; x < m; x += NT) data[x] = G[a + x];
         __syncthreads();
         E* X = reinterpret_cast<E*>(reinterpret_cast<uintptr_t>(data) - a * EB);  // absolute positions
@@ -688,7 +733,9 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_ipsc_small(IpscParams P, c
                 for (uint32_t i = tid; i < k; i += NT) slots[(uint64_t)d * k + i] = cur[i];
             __syncthreads();
         }
+        if (tk) P.clk[1] = clock64();
         fine_seg<EB, NT, true>(X, P, a, m, cur, Sb, F, &s_R, &s_prefix);
+        if (tk) P.clk[5] = clock64();
         // children: Fisher-Yates leaves in shared memory, longer ones to the next level
         const PhiloxKey key = make_key(P.seed);
         for (uint32_t c = tid; c < k; c += NT) {
@@ -711,8 +758,10 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_ipsc_small(IpscParams P, c
             }
         }
         __syncthreads();
+        if (tk) P.clk[6] = clock64();
         for (uint64_t x = tid; x < m; x += NT) G[a + x] = data[x];
         __syncthreads();
+        if (tk) P.clk[7] = clock64();
     }
 }
 

@@ -827,6 +827,8 @@ static shuf_status enqueue_ipsc(shuf_plan_s* p, void* ptr, void* aux, cudaStream
     P.max_next = l.max_segs;
     P.hdr = hdr;
     P.run_leaves = (uint32_t)run_leaves;
+    if (const char* dbg = std::getenv("SHUF_DBG"))
+        if (std::atoi(dbg) & 128) P.clk = hdr->clk;
     uint32_t rs_grid = 2u * (uint32_t)p->sms;  // SHUF_IPSC_RSGRID=<CTAs per SM> (experiments)
     if (const char* g = std::getenv("SHUF_IPSC_RSGRID")) rs_grid = (uint32_t)std::atoi(g) * (uint32_t)p->sms;
     uint32_t tsmall = 0;  // (the capacity's tree depth; launches size their own)

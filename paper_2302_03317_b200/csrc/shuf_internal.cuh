@@ -243,6 +243,7 @@ struct IpscParams {
     uint32_t* next_cnt;
     uint64_t max_next;
     Header* hdr;
+    long long* clk;      // SHUF_DBG & 128: phase clocks of CTA 0's first small segment (hdr->clk)
 };
 
 // ------------------------------------------------------ host launchers ---

@@ -27,3 +27,7 @@ for r in range(a.reps):
     shuf.shuf_run_ipsc(plan, x, aux)
     torch.cuda.synchronize()
     print(f"rep {r}: {1e3 * (time.perf_counter() - t0):.2f} ms, err {shuf.shuf_last_device_error(plan)}", flush=True)
+if os.environ.get("SHUF_DBG"):
+    c = shuf.shuf_debug_clocks(plan)[:8]
+    names = ["load", "RS tree", "R+multinomial", "TwoSweep", "stash FY", "children", "store"]
+    print("small-kernel phases (cycles):", {n: c[i + 1] - c[i] for i, n in enumerate(names)})
