@@ -606,48 +606,39 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
         __syncthreads();
         if (tk && P.clk[4] == 0) P.clk[4] = clock64();
     }
-    for (uint64_t stamp = 1; top >= 1; ++stamp) {
-        const uint64_t o = tid;
-        const bool valid = top >= o + 1;
+    // CTA rounds of up to NT steps (32-bit tables in the hash region, reset every
+    // round): hk/hv = open-addressing map partner -> min order; win[d] = min order
+    // of a step whose partner is the round's index top - d.
+    uint32_t* hk = reinterpret_cast<uint32_t*>(hkey);
+    uint32_t* hv = hk + H;
+    uint32_t* win = hv + H;
+    for (uint32_t x = tid; x < H; x += NT) {
+        hk[x] = 0xFFFFFFFFu;
+        hv[x] = 0xFFFFFFFFu;
+    }
+    for (uint32_t x = tid; x < NT; x += NT) win[x] = 0xFFFFFFFFu;
+    __syncthreads();
+    while (top >= 1) {
+        const uint32_t o = tid;
+        const bool valid = top >= (uint64_t)o + 1;
         const uint32_t i = valid ? (uint32_t)(top - o) : 0u;
         const uint32_t j = valid ? ipsc_draw(key, TAG_IPSC_FY, i, 0u, P.level, a, i + 1) : 0u;
         if (tid == 0) *s_prefix = (uint32_t)(top < NT ? top : NT);
-        if (valid) {  // insert (j, order o): min order per partner
-            const uint64_t mk = (stamp << 32) | j;
+        uint32_t hslot = 0;
+        if (valid) {
+            const uint64_t d = top - j;
+            if (d < NT && d > o) atomicMin(&win[d], o);
             uint32_t h = fy_hash(j, H);
             for (;;) {
-                const uint64_t k0 = hkey[h];
-                if (k0 == mk) break;
-                if ((k0 >> 32) != stamp) {
-                    const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(&hkey[h]), k0, mk);
-                    if (prev == k0 || prev == mk) break;
-                    continue;
-                }
+                const uint32_t prev = atomicCAS(&hk[h], 0xFFFFFFFFu, j);
+                if (prev == 0xFFFFFFFFu || prev == j) break;
                 h = (h + 1) & (H - 1u);
             }
-            atomicMax(reinterpret_cast<unsigned long long*>(&hval[h]), (stamp << 32) | (0xFFFFFFFFull - o));
+            atomicMin(&hv[h], o);
+            hslot = h;
         }
         __syncthreads();
-        if (valid) {
-            bool conflict = false;
-            const uint32_t qs[2] = {i, j};
-#pragma unroll
-            for (int z = 0; z < 2; ++z) {  // an earlier step with partner i, or with my partner j
-                const uint64_t mk = (stamp << 32) | qs[z];
-                uint32_t h = fy_hash(qs[z], H);
-                for (;;) {
-                    const uint64_t k0 = hkey[h];
-                    if (k0 == mk) {
-                        const uint64_t vv = hval[h];
-                        if ((vv >> 32) == stamp && 0xFFFFFFFFull - (vv & 0xFFFFFFFFull) < o) conflict = true;
-                        break;
-                    }
-                    if ((k0 >> 32) != stamp) break;
-                    h = (h + 1) & (H - 1u);
-                }
-            }
-            if (conflict) atomicMin(s_prefix, (uint32_t)o);
-        }
+        if (valid && (win[o] < o || hv[hslot] < o)) atomicMin(s_prefix, o);
         __syncthreads();
         const uint32_t pre = *s_prefix;
         if (valid && o < pre && i != j) {
@@ -656,6 +647,11 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
             X[pi] = X[pj];
             X[pj] = t0;
         }
+        if (valid) {
+            hk[hslot] = 0xFFFFFFFFu;
+            hv[hslot] = 0xFFFFFFFFu;
+        }
+        win[o] = 0xFFFFFFFFu;
         __syncthreads();
         top -= pre;
     }
