@@ -562,7 +562,8 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
     __syncthreads();
     // stash shuffle: Fisher-Yates on V[t] = X[p_t], rounds of conflict-free prefixes
     uint64_t top = R ? R - 1 : 0;
-    if (WARP_SWEEP) {  // warp 0, rounds of <= 32 steps; conflicts found by match_any and an OR-reduction
+    constexpr bool kWarpFy = true;  // shared-memory data: warp-0 rounds (CTA rounds measured 1.8x slower, r03g)
+    if (WARP_SWEEP && kWarpFy) {  // warp 0, rounds of <= 32 steps; conflicts found by match_any and an OR-reduction
         // positions p_t - a as u16 in the (here unused) hash region when they fit
         uint16_t* posT = reinterpret_cast<uint16_t*>(hkey);
         const bool tab = R <= 8u * H && m <= 65536u;
