@@ -537,10 +537,10 @@ __device__ __forceinline__ void s_place(const XView<EB>& V, const XItem& it, uns
         const uint32_t b = valid ? (uint32_t)dp[i] : 0u;
         uint32_t slot;
         if (ORD && NARROW) {
-            slot = atomicAdd(&Tw[b], valid ? 1u : 0u);
+            slot = atomicAdd(&Tw[valid ? b : (lane < kw ? lane : 0u)], valid ? 1u : 0u);  // idle lanes: +0, spread over banks
         } else if (ORD) {
             const uint32_t shb = (b & 1u) << 4;
-            slot = (atomicAdd(&Tw[b >> 1], valid ? (1u << shb) : 0u) >> shb) & 0xFFFFu;
+            slot = (atomicAdd(&Tw[valid ? b >> 1 : (lane < kw ? lane : 0u)], valid ? (1u << shb) : 0u) >> shb) & 0xFFFFu;
         } else if (NARROW) {
             const uint32_t peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu);
             slot = valid ? Tw[b] + __popc(peers & lanemask_lt()) : 0u;
