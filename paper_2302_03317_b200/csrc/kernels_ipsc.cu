@@ -506,10 +506,22 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
     for (uint32_t r = tid; r < (uint32_t)R; r += NT)
         atomicAdd(&cnt[ipsc_draw(key, TAG_IPSC_FM, r, 0u, P.level, a, k)], 1u);
     __syncthreads();
-    if (tid == 0) {  // D_i = sum_{j<=i} (n^f_j - c_j)  (Lemma 4)
-        int64_t D = 0;
-        for (uint32_t i = 0; i < k; ++i) {
+    // D_i = sum_{j<=i} (n^f_j - c_j)  (Lemma 4): warp 0 scans, lane l owning buckets [l*per, (l+1)*per)
+    if (tid < 32) {
+        const uint32_t per = (k + 31u) >> 5, i0 = tid * per, i1 = min(k, i0 + per);
+        int64_t part = 0;
+        for (uint32_t i = i0; i < i1; ++i) {
             nf[i] = s[i] - b[i] + cnt[i];
+            part += (int64_t)nf[i] - (int64_t)(e[i] - b[i]);
+        }
+        int64_t incl = part;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (tid >= (uint32_t)o) incl += t;
+        }
+        int64_t D = incl - part;
+        for (uint32_t i = i0; i < i1; ++i) {
             D += (int64_t)nf[i] - (int64_t)(e[i] - b[i]);
             Dp[i] = D;
         }
@@ -549,15 +561,28 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
     for (uint32_t i = tid; i + 1 < k; i += NT) e[i] = b[i + 1];
     __syncthreads();
     if (tk && P.clk[3] == 0) P.clk[3] = clock64();
-    if (tid == 0) {
-        uint64_t t = 0;
-        for (uint32_t i = 0; i < k; ++i) {
-            if (s[i] < b[i] || s[i] > e[i] || e[i] - b[i] != nf[i]) ipsc_latch(P.hdr, 8u);  // final sizes reached
+    if (tid < 32) {  // cum = exclusive prefix of the staged counts (warp 0), and the final sizes reached
+        const uint32_t per = (k + 31u) >> 5, i0 = tid * per, i1 = min(k, i0 + per);
+        uint64_t part = 0;
+        for (uint32_t i = i0; i < i1; ++i) {
+            if (s[i] < b[i] || s[i] > e[i] || e[i] - b[i] != nf[i]) ipsc_latch(P.hdr, 8u);
+            part += e[i] - s[i];
+        }
+        uint64_t incl = part;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (tid >= (uint32_t)o) incl += t;
+        }
+        uint64_t t = incl - part;
+        for (uint32_t i = i0; i < i1; ++i) {
             cum[i] = t;
             t += e[i] - s[i];
         }
-        cum[k] = t;
-        if (t != R) ipsc_latch(P.hdr, 8u);
+        if (tid == 31) {
+            cum[k] = incl;
+            if (incl != R) ipsc_latch(P.hdr, 8u);
+        }
     }
     __syncthreads();
     // stash shuffle: Fisher-Yates on V[t] = X[p_t], rounds of conflict-free prefixes
@@ -581,8 +606,8 @@ __device__ void fine_seg(typename ElemT<EB>::type* X, const IpscParams& P, uint6
                 // the draws of the next 32 steps, assuming this round runs all 32 (the usual case)
                 const uint32_t tq = tp >= 32u ? tp - 32u : 0u;
                 const uint32_t jspec = tq >= lane + 1 ? ipsc_draw(key, TAG_IPSC_FY, tq - lane, 0u, P.level, a, tq - lane + 1) : 0u;
-                const unsigned long long mk = valid ? (unsigned long long)j : (1ull << 32) | lane;
-                bool conflict = (__match_any_sync(0xFFFFFFFFu, mk) & lt) != 0;  // an earlier step shares my partner
+                // (j <= i < R < 2^31: idle lanes match nothing)
+                bool conflict = (__match_any_sync(0xFFFFFFFFu, valid ? j : 0xFFFFFFFFu - lane) & lt) != 0;
                 // an earlier step's partner is my own index: lane l' with j = tp - l (l > l') hits lane l
                 const uint32_t d = tp - j;
                 const uint32_t hit = __reduce_or_sync(0xFFFFFFFFu, valid && d < 32u && d > lane ? 1u << d : 0u);
