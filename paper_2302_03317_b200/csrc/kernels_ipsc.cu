@@ -39,6 +39,8 @@
 // at once.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "block_ops.cuh"
 #include "shuf_internal.cuh"
 
@@ -833,11 +835,17 @@ template <int EB>
 static cudaError_t rs_launch_eb(const IpscParams& P, uint32_t nwork, bool merge, bool wide, uint32_t grid,
                                 cudaStream_t s) {
     if (wide) return merge ? rs_launch<EB, 1024, true>(P, nwork, nwork, s) : rs_launch<EB, 1024, false>(P, nwork, nwork, s);
-    (void)grid;
+    static const int mode = [] {  // SHUF_IPSC_RSMODE (experiments): 0 = one warp per node, 1 = persistent
+        const char* e = std::getenv("SHUF_IPSC_RSMODE");  // 256-thread CTAs (default), 2 = 1024-thread CTAs
+        return e ? std::atoi(e) : 1;
+    }();
+    if (mode == 1) return merge ? rs_launch<EB, 256, true>(P, nwork, grid, s) : rs_launch<EB, 256, false>(P, nwork, grid, s);
+    if (mode == 2) return merge ? rs_launch<EB, 1024, true>(P, nwork, grid, s) : rs_launch<EB, 1024, false>(P, nwork, grid, s);
     return merge ? rs_warp_launch<EB, true>(P, nwork, s) : rs_warp_launch<EB, false>(P, nwork, s);
 }
 
-// wide: one 1024-thread CTA per node (few nodes); otherwise `grid` persistent 256-thread CTAs.
+// wide: one 1024-thread CTA per node (few nodes); otherwise `grid` persistent 256-thread CTAs walking the
+// work list in order (measured faster than one warp per node, r03n/r03o).
 cudaError_t launch_ipsc_rs(const IpscParams& P, uint32_t eb, uint32_t nwork, bool merge, bool wide, uint32_t grid,
                            cudaStream_t s) {
     if (nwork == 0) return cudaSuccess;

@@ -829,8 +829,9 @@ static shuf_status enqueue_ipsc(shuf_plan_s* p, void* ptr, void* aux, cudaStream
     P.run_leaves = (uint32_t)run_leaves;
     if (const char* dbg = std::getenv("SHUF_DBG"))
         if (std::atoi(dbg) & 128) P.clk = hdr->clk;
-    uint32_t rs_grid = 2u * (uint32_t)p->sms;  // SHUF_IPSC_RSGRID=<CTAs per SM> (experiments)
-    if (const char* g = std::getenv("SHUF_IPSC_RSGRID")) rs_grid = (uint32_t)std::atoi(g) * (uint32_t)p->sms;
+    // RoughScatter: 8 persistent CTAs per SM (HOT: 1/2/3/4/6/8 per SM -> 248/213/206/203/199/196 ms, r03n/r03o)
+    int rs_per_sm = 8;  // SHUF_IPSC_RSGRID=<CTAs per SM> (experiments)
+    if (const char* g = std::getenv("SHUF_IPSC_RSGRID")) rs_per_sm = std::atoi(g);
     uint32_t tsmall = 0;  // (the capacity's tree depth; launches size their own)
     const uint32_t cap = std::getenv("SHUF_IPSC_NOSMALL") ? 0u : ipsc_small_cap(p->k, p->eb, &tsmall);
     IpscSeg* d_bsegs = reinterpret_cast<IpscSeg*>(ax + l.bsegs);
@@ -911,7 +912,7 @@ static shuf_status enqueue_ipsc(shuf_plan_s* p, void* ptr, void* aux, cudaStream
                 const uint32_t nw = wofs[q + 1] - wofs[q];
                 P.work = d_work + wofs[q];
                 const bool wide = nw < (uint32_t)p->sms;
-                LAUNCH(SHUF_K_SCATTER, launch_ipsc_rs(P, p->eb, nw, q > 0, wide, rs_grid, st));
+                LAUNCH(SHUF_K_SCATTER, launch_ipsc_rs(P, p->eb, nw, q > 0, wide, (uint32_t)rs_per_sm * (uint32_t)p->sms, st));
             }
             LAUNCH(SHUF_K_FINISH, launch_ipsc_fine(P, p->eb, (uint32_t)bs.size(), st));
             LAUNCH(SHUF_K_PLAN, launch_ipsc_children(P, (uint32_t)bs.size(), st, p->grid_small));
