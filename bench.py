@@ -252,7 +252,8 @@ def run_sharded(args, w, rank, world, local, dev):
                        "seed": w.seed, "l2": "inputs larger than L2 (no flush)",
                        "parallelism": f"sharded x{world} (level-0 all-to-all-v over NCCL)", "mode": "sharded",
                        "rank0_owned": info.get("m"), "rank0_p2p_pieces": info.get("pieces")},
-            "e2e": None, "roofline": None, "cpu_baseline": None,
+            "e2e": None, "roofline": None,
+            "cpu_baseline": None if args.no_cpu_baseline else cpu_baseline(w, min(args.cpu_sample, w.n)),
             "gpu_launches": info.get("launches", 0) * args.steps, "clocks": clk.summary(), "device": device_facts(dev),
         }
         print(json.dumps(line), flush=True)
@@ -271,15 +272,18 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(w, n_s):
+def cpu_baseline(w, n_s, mode="stable"):
+    """The oracle as it stands on a bounded prefix of the workload: D6 (oracle.shuffle), or
+    D10 (oracle.ipsc_shuffle) for --mode ipsc."""
     import oracle
     a = synth.make_input_np(w, n=n_s)
+    fn, what = (oracle.ipsc_shuffle, "IpSc (D10)") if mode == "ipsc" else (oracle.shuffle, "D6")
     t0 = time.perf_counter()
-    oracle.shuffle(a, w.k, w.L, w.seed)
+    fn(a, w.k, w.L, w.seed)
     dt = time.perf_counter() - t0
     return {"value": n_s / dt, "unit": "elements/s", "cores": 1, "kind": "oracle",
             "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
-            "sample": f"one oracle shuffle of the first {n_s} elements of the workload "
+            "sample": f"one oracle {what} shuffle of the first {n_s} elements of the workload "
                       f"({w.note}, k={w.k}, L={w.L}, seed={w.seed}); {dt:.1f} s on 1 host core"}
 
 
@@ -485,7 +489,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_gpu_baselines and d_off is None:
         gbase = gpu_baselines(x, w.n, ms, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(w if w.kind != "segmented" else synth.WORKLOADS["c1"], min(args.cpu_sample, w.n))
+        cpu = cpu_baseline(w if w.kind != "segmented" else synth.WORKLOADS["c1"], min(args.cpu_sample, w.n),
+                           "ipsc" if ipsc else "stable")
 
     if rank == 0:
         line = {
