@@ -70,6 +70,8 @@ FULL = [
     (1_000_003, 256, 4096, 9, 4),
     (4_000_037, 256, 2048, 10, 8),
     (500_000, 1024, 2048, 11, 16),
+    (20_000_003, 256, 2048, 3, 8),      # config-3 shape (u64, L = 2048), three IpSc levels
+    (8_000_000, 1024, 2048, 11, 16),    # config-4 shape (16-byte records, k = 1024)
 ]
 
 
