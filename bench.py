@@ -310,6 +310,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 25)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-buffers", type=int, default=2,
+                    help="device buffers rotating through the e2e pipeline (2, 3: 105 ms; 4: 119 ms on HOT, r03x)")
     ap.add_argument("--no-gpu-baselines", action="store_true",
                     help="skip the library GPU shuffles timed beside ours (SURVEY 8(f) NEXT-4)")
     args = ap.parse_args()
@@ -444,11 +446,26 @@ def main():
         host_in.copy_(x)
         host_out = torch.empty_like(host_in, pin_memory=True)
         nbytes = x.numel() * x.element_size()
-        xbuf = [x, torch.empty_like(x)]
+        NB = max(2, args.e2e_buffers)
+        xbuf = [x] + [torch.empty_like(x) for _ in range(NB - 1)]
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_comp = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_comp = [torch.cuda.Event() for _ in range(NB)]
+        ev_out = [torch.cuda.Event() for _ in range(NB)]
+        # the link alone, each direction (context for the e2e number)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s_in):
+            g0.record(s_in)
+            xbuf[1].copy_(host_in, non_blocking=True)
+            g1.record(s_in)
+        torch.cuda.synchronize(dev)
+        h2d_gbps = nbytes / (g0.elapsed_time(g1) / 1e3) / 1e9
+        with torch.cuda.stream(s_out):
+            g0.record(s_out)
+            host_out.copy_(xbuf[1], non_blocking=True)
+            g1.record(s_out)
+        torch.cuda.synchronize(dev)
+        d2h_gbps = nbytes / (g0.elapsed_time(g1) / 1e3) / 1e9
 
         def run_on(xd):
             if d_off is None:
@@ -462,10 +479,10 @@ def main():
         s_in.wait_event(f0)
         s_out.wait_event(f0)
         for i in range(args.e2e_steps):
-            d = i % 2
+            d = i % NB
             with torch.cuda.stream(s_in):
-                if i >= 2:
-                    s_in.wait_event(ev_out[d])  # step i-2's download has read buffer d
+                if i >= NB:
+                    s_in.wait_event(ev_out[d])  # step i-NB's download has read buffer d
                 xbuf[d].copy_(host_in, non_blocking=True)
                 ev_in[d].record(s_in)
             stream.wait_event(ev_in[d])
@@ -475,13 +492,15 @@ def main():
                 s_out.wait_event(ev_comp[d])
                 host_out.copy_(xbuf[d], non_blocking=True)
                 ev_out[d].record(s_out)
-        stream.wait_event(ev_out[(args.e2e_steps - 1) % 2])
+        stream.wait_event(ev_out[(args.e2e_steps - 1) % NB])
         f1.record(stream)
         barrier()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
         e2e = {"value": job_value(w.n, world, e2e_ms), "unit": "elements/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-               "overlap": "uploads, shuffles and downloads of consecutive steps overlap on three streams"}
+               "overlap": f"uploads, shuffles and downloads of consecutive steps overlap on three streams, "
+                          f"{NB} device buffers",
+               "link_alone_GBps": {"h2d": round(h2d_gbps, 1), "d2h": round(d2h_gbps, 1)}}
         del host_in, host_out, xbuf
 
     cpu = None
