@@ -99,9 +99,9 @@ def _worker(rank, world, port, n, k, L, seed, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,k", [(100_003, 256), (50_000, 7)])
-def test_two_gloo_ranks_exchange_gives_oracle_level0(n, k):
-    world, port = 2, _free_port()
+@pytest.mark.parametrize("n,k,world", [(100_003, 256, 2), (50_000, 7, 2), (60_001, 16, 3)])
+def test_gloo_ranks_exchange_gives_oracle_level0(n, k, world):
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, k, 64, 17, q)) for r in range(world)]
@@ -112,4 +112,26 @@ def test_two_gloo_ranks_exchange_gives_oracle_level0(n, k):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert [r[3] for r in res] == [True] * world
-    assert res[0][1] == 0 and res[0][2] + res[1][2] == n and res[1][1] == res[0][2]
+    at = 0
+    for _, base, m, _ in res:  # the owned ranges tile [0, n) in rank order
+        assert base == at
+        at += m
+    assert at == n
+
+
+def test_capacity_bounds_every_owner():
+    """A rank's buffers (capacity) hold its slice and, with a 12-sigma margin, its buckets."""
+    rng = np.random.default_rng(3)
+    for n, world, k in [(1 << 20, 2, 256), (1 << 22, 8, 1024), (10_007, 3, 7)]:
+        cap = sharded.capacity(n, world, k)
+        assert cap >= -(-n // world)
+        for _ in range(20):
+            counts = rng.multinomial(n, [1.0 / k] * k)
+            for r in range(world):
+                b0, b1 = sharded.owned_buckets(k, world, r)
+                assert int(counts[b0:b1].sum()) <= cap
+
+
+def test_k_smaller_than_world_is_rejected():
+    with pytest.raises(ValueError):
+        sharded.ShardedShuffle(1000, 4, 2, 16, 1, 0, 4, device="cpu")
