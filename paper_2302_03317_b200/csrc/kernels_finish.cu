@@ -11,6 +11,9 @@ void* finish_children_kernel_eb16(bool seg, bool narrow, bool ord);
 void* finish_ip_kernel_eb4(bool narrow, bool ord);
 void* finish_ip_kernel_eb8(bool narrow, bool ord);
 void* finish_ip_kernel_eb16(bool narrow, bool ord);
+void* finish_stream_kernel_eb4(bool narrow, bool ord);
+void* finish_stream_kernel_eb8(bool narrow, bool ord);
+void* finish_stream_kernel_eb16(bool narrow, bool ord);
 cudaError_t launch_copy_big_eb4(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_copy_big_eb8(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_copy_big_eb16(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
@@ -18,7 +21,32 @@ cudaError_t launch_copy_big_eb16(const RunParams& rp, const LevelParams& lp, cud
 uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t) {
     return finish_layout(S_fuse, eb, k).total;
 }
+uint32_t finish_stream_smem_bytes(uint32_t S, uint32_t eb, uint32_t k) { return finish_layout(S, eb, k, true).total; }
 uint32_t finish_max_elems(uint32_t, uint32_t) { return 65535u; }
+
+static void* fin_stream(uint32_t eb, bool narrow, bool ord) {
+    switch (eb) {
+    case 4: return finish_stream_kernel_eb4(narrow, ord);
+    case 8: return finish_stream_kernel_eb8(narrow, ord);
+    default: return finish_stream_kernel_eb16(narrow, ord);
+    }
+}
+
+cudaError_t configure_finish_stream(uint32_t eb, uint32_t smem) {
+    for (int nr = 0; nr < 2; ++nr)
+        for (int o = 0; o < 2; ++o) {
+            cudaError_t e = cudaFuncSetAttribute(fin_stream(eb, nr, o), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e) return e;
+        }
+    return cudaSuccess;
+}
+
+cudaError_t launch_finish_stream(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
+    const uint32_t smem = finish_stream_smem_bytes(rp.S_stream, rp.eb, rp.k);
+    void* args[] = {(void*)&rp, (void*)&lp};
+    return cudaLaunchKernel(fin_stream(rp.eb, rp.bp.narrow != 0, rp.rank_ordered != 0), dim3(grid), dim3(NTF), args,
+                            smem, s);
+}
 uint32_t finish_smem_budget(uint32_t) { return kSmemLimit; }
 
 static void* fin_fn(uint32_t eb, bool seg, bool narrow, bool ord) {

@@ -64,7 +64,9 @@ struct FinishLayout {
     uint32_t in, out, draws, C, bst, wsum, front0, front1, bar, total;
 };
 
-__host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, uint32_t k) {
+// stream: the single-buffer layout of k_finish_stream (the item's first
+// in-smem level reads it straight from the level's output buffer: no IN).
+__host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, uint32_t k, bool stream = false) {
     FinishLayout f;
     uint32_t off = 0;
     auto take = [&off](uint32_t bytes) {
@@ -73,7 +75,7 @@ __host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, u
         return at;
     };
     take(sizeof(FinCtl));  // offset 0
-    f.in = take(S * eb + 32);
+    f.in = take(stream ? 16u : S * eb + 32);
     f.out = take(S * eb + 32);
     f.draws = take(2 * S + 64);  // bucket draws (u8 / u16)
     f.C = take(finish_rank_warps(k) * ((k + 1) / 2) * 4);
@@ -91,6 +93,8 @@ __host__ __device__ inline FinishLayout finish_layout(uint32_t S, uint32_t eb, u
 struct Fin {
     FinishLayout f;
     __device__ __forceinline__ explicit Fin(const RunParams& rp) : f(finish_layout(rp.S_fuse, rp.eb, rp.k)) {}
+    __device__ __forceinline__ Fin(const RunParams& rp, bool stream)
+        : f(finish_layout(stream ? rp.S_stream : rp.S_fuse, rp.eb, rp.k, stream)) {}
     __device__ __forceinline__ FinCtl* ctl() const { return reinterpret_cast<FinCtl*>(fsm); }
     __device__ __forceinline__ unsigned char* in() const { return fsm + f.in; }
     __device__ __forceinline__ unsigned char* out() const { return fsm + f.out; }
@@ -422,6 +426,7 @@ struct ChildIter {
     const RunParams* rp;
     const LevelParams* lp;
     uint32_t groups;
+    bool stream = false;  // k_finish_stream: the children with S_fuse < len <= S_stream
     __device__ __forceinline__ void load_unit(FinCtl* ctl) const {  // warp 0, all lanes
         const uint32_t lane = threadIdx.x & 31u;
         const SegDesc sg = lp->segs[(uint32_t)(ctl->u / groups)];
@@ -448,11 +453,15 @@ struct ChildIter {
             const uint32_t b0 = (uint32_t)(ctl->u % groups) * kUnit;
             for (uint32_t b = ctl->b; b < ctl->bend; ++b) {
                 const uint64_t s0 = ctl->ub[b - b0], len = ctl->ub[b - b0 + 1] - s0;
-                if (len == 0 || len > rp->S_fuse) continue;
-                if (rp->leafk && len <= rp->L) continue;  // the leaf kernel's
-                if (lp->dst == rp->buf0 && !item_permutes(*rp, (uint32_t)len, lvl)) continue;
-                // children finished by k_finish_fast carry flag 0
-                if (rp->fast && rp->flags[(ctl->u / groups) * rp->k + b] == 0) continue;
+                if (stream) {
+                    if (len <= rp->S_fuse || len > rp->S_stream || lvl >= rp->max_levels) continue;
+                } else {
+                    if (len == 0 || len > rp->S_fuse) continue;
+                    if (rp->leafk && len <= rp->L) continue;  // the leaf kernel's
+                    if (lp->dst == rp->buf0 && !item_permutes(*rp, (uint32_t)len, lvl)) continue;
+                    // children finished by k_finish_fast carry flag 0
+                    if (rp->fast && rp->flags[(ctl->u / groups) * rp->k + b] == 0) continue;
+                }
                 __syncwarp();
                 if (lane == 0) {
                     Item& it = ctl->items[slot];
@@ -684,6 +693,66 @@ __global__ void __launch_bounds__(NTF, 1)
     __syncthreads();
     SegIter iter{&rp, off};
     run_items<EB, NARROW, ORD>(rp, F, iter, rp.buf0);
+}
+
+// Single-buffer finish of the children with S_fuse < len <= S_stream (items
+// too long for IN + OUT): the item's in-smem level reads its elements straight
+// from the level's output buffer (coalesced, in position order) and places
+// them into OUT; its children are leaves (the plan enables the stream only when
+// len / k stays far below L), Fisher-Yates'd in OUT; OUT goes to
+// ptr with one bulk store.  A child longer than L (not seen in any plan that
+// enables the stream: > 12 sigma) latches SHUF_ERR_DEPTH.
+template <int EB, bool NARROW, bool ORD>
+__global__ void __launch_bounds__(NTF, 1) k_finish_stream(RunParams rp, LevelParams lp) {
+    const uint32_t groups = (rp.k + kUnit - 1) / kUnit;
+    const uint64_t units = (uint64_t)lp.ctr->nseg * groups;
+    if (blockIdx.x >= units || lp.ctr->nstream == 0) return;
+    const Fin F(rp, true);
+    fin_init(F);
+    ChildIter iter{&rp, &lp, groups};
+    iter.stream = true;
+    FinCtl* ctl = F.ctl();
+    const uint32_t tid = threadIdx.x;
+    if (tid < 32) {
+        if (tid == 0) {
+            ctl->u = blockIdx.x;
+            ctl->units = units;
+        }
+        __syncwarp();
+        iter.load_unit(ctl);
+    }
+    __syncthreads();
+    uint32_t fy_local = 0;
+    for (;;) {
+        if (tid < 32) iter.next(ctl, 0);
+        __syncthreads();
+        if (!ctl->have[0]) break;
+        const Item it = ctl->items[0];
+        const uint32_t off = (uint32_t)((it.start * EB) & 15u);
+        unsigned char* out = F.out() + off;
+        const PhiloxKey key = make_key(it.key);
+        const uint64_t P0 = it.start - it.origin;
+        if (tid == 0) {
+            ctl->st_finished += it.len;
+            bulk_wait_read0();  // OUT was last read by the previous item's bulk store
+        }
+        __syncthreads();
+        smem_level<EB, NARROW, ORD>(rp, F, lp.dst + it.start * EB, out, 0, it.len, P0, it.level, key, false);
+        if (tid == 0) ctl->nfront = 0;
+        __syncthreads();
+        handle_children<EB>(rp, F, out, 0, it.len, P0, it.level, key, F.front(0), fy_local);
+        __syncthreads();
+        if (tid == 0 && ctl->nfront) atomicCAS(&rp.hdr->error, 0u, 5u /*SHUF_ERR_DEPTH*/);
+        item_store<EB>(it, rp.buf0, F.out());  // (fences every writer, then one bulk store)
+    }
+    for (int o = 16; o > 0; o >>= 1) fy_local += __shfl_xor_sync(0xFFFFFFFFu, fy_local, o);
+    if ((tid & 31u) == 0 && fy_local) atomicAdd((unsigned long long*)&rp.hdr->fy_elems, (unsigned long long)fy_local);
+    if (tid == 0) {
+        atomicAdd((unsigned long long*)&rp.hdr->finished, ctl->st_finished);
+        for (uint32_t l = 0; l < 32; ++l)
+            if (ctl->st_smem[l]) atomicAdd((unsigned long long*)&rp.hdr->scattered_smem[l], ctl->st_smem[l]);
+        bulk_wait0();
+    }
 }
 
 // Debug level limit: children longer than S_fuse produced by the last level

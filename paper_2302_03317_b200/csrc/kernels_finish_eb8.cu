@@ -18,6 +18,11 @@ void* finish_ip_kernel_eb8(bool narrow, bool ord) {
     return narrow ? (void*)k_finish_ipchildren<8, true, false> : (void*)k_finish_ipchildren<8, false, false>;
 }
 
+void* finish_stream_kernel_eb8(bool narrow, bool ord) {
+    if (ord) return narrow ? (void*)k_finish_stream<8, true, true> : (void*)k_finish_stream<8, false, true>;
+    return narrow ? (void*)k_finish_stream<8, true, false> : (void*)k_finish_stream<8, false, false>;
+}
+
 cudaError_t launch_copy_big_eb8(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     k_copy_big<8><<<grid, 256, 0, s>>>(rp, lp);
     return cudaGetLastError();

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
     if (gtid() == 0) {
         lp.ctr->scan_ticket = 0;
         lp.ctr->nfuse = 0;
+        lp.ctr->nstream = 0;
         // (the next level's segment counters are reset by k_scan: this kernel may
         // run while the previous level's kernels still read that slot)
     }
@@ -302,6 +303,10 @@ __global__ void k_plan(RunParams rp, LevelParams lp) {
                     else latch_error(rp.hdr, 4u);
                 }
             }
+            continue;
+        }
+        if (rp.S_stream && len <= rp.S_stream) {  // k_finish_stream takes it (single buffer)
+            atomicAdd(&lp.ctr->nstream, 1u);
             continue;
         }
         if (next >= rp.max_levels) continue;  // debug level limit: copied out by k_finish_children

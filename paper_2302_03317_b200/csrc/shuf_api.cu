@@ -31,6 +31,7 @@ struct shuf_plan_s {
     uint32_t eb, k, L;
     uint64_t seed;
     uint32_t S_fuse, chunk, levels, fin_nbuf;
+    uint32_t S_stream;  // children with S_fuse < len <= S_stream: k_finish_stream (0: none)
     int defer_planned;  // SHUF_DEFER=1 at plan time: item records are laid out
     ScratchLayout lay;  // shuf_run's layout (one level-0 segment)
     IpAuxLayout ipl;
@@ -94,11 +95,11 @@ static uint32_t pick_s_fuse(uint32_t eb, uint32_t k, uint32_t L, uint32_t* nbuf)
 // 6-sigma binomial margin per level, plus one spare level (a rarer outlier
 // child simply takes the spare level; only one that outlives the spare
 // level too raises SHUF_ERR_DEPTH).
-static uint32_t plan_levels(uint64_t n, uint32_t k, uint32_t S_fuse) {
+static uint32_t plan_levels(uint64_t n, uint32_t k, uint32_t S_fuse, uint32_t S_eff) {
     if (n <= S_fuse) return 0;
     double m = (double)n;
     uint32_t g = 0;
-    while (m > S_fuse && g < kMaxLevels) {
+    while (m > S_eff && g < kMaxLevels) {
         ++g;
         double mu = m / k;
         m = mu + 6.0 * std::sqrt(mu) + 32.0;
@@ -158,7 +159,8 @@ static ScratchLayout compute_layout(const shuf_plan_s* p, uint64_t segs0, bool s
     ScratchLayout l{};
     const uint64_t n = p->n;
     std::vector<uint64_t> sc(p->levels + 1, 0), cc(p->levels + 1, 0);
-    if (p->levels) level_caps(n, p->k, p->S_fuse, p->chunk, p->levels, segs0, segmented, sc.data(), cc.data());
+    const uint32_t S_eff = p->S_stream ? p->S_stream : p->S_fuse;  // children above it take another HBM level
+    if (p->levels) level_caps(n, p->k, S_eff, p->chunk, p->levels, segs0, segmented, sc.data(), cc.data());
     for (int s = 0; s < 2; ++s) {
         l.seg_cap[s] = l.chunk_cap[s] = 1;
         for (uint32_t lv = (uint32_t)s; lv < p->levels; lv += 2) {
@@ -322,7 +324,20 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     C = align_up(C < T ? T : C, T);
     if (C > 0x40000000ull) C = 0x40000000ull;
     p->chunk = (uint32_t)C;
-    p->levels = plan_levels(n, k, S);
+    {  // single-buffer streaming finish (k_finish_stream) for children too long for the fused size,
+       // when their own children stay far below L (> 12 sigma); SHUF_STREAM=0 disables it
+        uint32_t Ss = 0;
+        for (uint32_t c = 65535u; c > S; c -= 64u)
+            if (finish_stream_smem_bytes(c, elem_bytes, k) <= kSmemLimit) {
+                Ss = c;
+                break;
+            }
+        const double mc = (double)Ss / k;
+        const char* se = std::getenv("SHUF_STREAM");
+        const bool on = !(se && se[0] == '0') && Ss >= S + S / 8 && mc + 12.0 * std::sqrt(mc) + 32.0 <= (double)L;
+        p->S_stream = on ? Ss : 0u;
+    }
+    p->levels = plan_levels(n, k, S, p->S_stream ? p->S_stream : S);
     {  // SHUF_LEVELS=<n>: fewer planned HBM levels (test hook for the device depth check)
         const char* le = std::getenv("SHUF_LEVELS");
         const long v = le ? std::atol(le) : -1;
@@ -403,6 +418,7 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     p->finish_smem = finish_smem_bytes(p->S_fuse, p->eb, p->k, p->fin_nbuf);
     p->scatter_smem = scatter_smem_bytes(p->eb, p->k);
     if ((e = configure_finish(p->finish_smem))) return e;
+    if (p->S_stream && (e = configure_finish_stream(p->eb, finish_stream_smem_bytes(p->S_stream, p->eb, p->k)))) return e;
     if ((e = configure_scatter(p->scatter_smem))) return e;
     // pipelined finish (kernels_fast.cu) for single-level items; SHUF_FAST_FINISH=0
     // leaves every item to the general finish kernel
@@ -580,6 +596,7 @@ static RunParams base_params(const shuf_plan_s* p, const ScratchLayout& lay, uns
     rp.k = p->k;
     rp.L = p->L;
     rp.S_fuse = p->S_fuse;
+    rp.S_stream = p->S_stream;
     rp.chunk = p->chunk;
     rp.max_levels = max_levels;
     rp.planned_levels = p->levels;
@@ -670,6 +687,7 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         LAUNCH(SHUF_K_SCATTER, launch_scatter(rp, lp, st, p->grid_scatter));
         if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast(rp, lp, st, p->grid_fast));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
+        if (p->S_stream) LAUNCH(SHUF_K_FINISH, launch_finish_stream(rp, lp, st, p->sms));
         if (p->leafk) LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->grid_leaf));
         if (lv + lv0 + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
     }
@@ -1000,6 +1018,7 @@ static shuf_status enqueue_inplace(shuf_plan_s* p, void* ptr, void* aux, cudaStr
     rp.k = p->k;
     rp.L = p->L;
     rp.S_fuse = p->S_fuse;
+    rp.S_stream = p->S_stream;
     rp.chunk = p->chunk;
     rp.max_levels = max_levels;
     rp.planned_levels = p->levels;

@@ -46,7 +46,9 @@ struct LevelCounters {
     uint32_t nseg;
     uint32_t nchunk;
     uint32_t scan_ticket;
-    uint32_t nfuse;  // children of this level in the fused list (RunParams::fused)
+    uint32_t nfuse;    // children of this level in the fused list (RunParams::fused)
+    uint32_t nstream;  // children of this level for k_finish_stream
+    uint32_t pad;
 };
 
 struct Header {
@@ -117,6 +119,7 @@ struct RunParams {
     // Sharded problem (NEXT-3, shuf_shard_*): buf0 holds a contiguous slice of one
     // problem of global positions [seg_base, seg_base + n); its segments are
     // children at level first_level, keyed K(seed, 0), positions global.
+    uint32_t S_stream;      // children with S_fuse < len <= S_stream: k_finish_stream (0: none)
     uint32_t shard;         // 1: the above; 0: single problem / user segments (D7)
     uint32_t first_level;   // level of the initial segments (0 unless shard)
     uint64_t seg_base;      // global position of buf0[0] (shard only)
@@ -270,6 +273,9 @@ cudaError_t launch_finish_segments(const RunParams& rp, const uint64_t* d_offset
                                    cudaStream_t s, int grid);
 uint32_t finish_smem_bytes(uint32_t S_fuse, uint32_t eb, uint32_t k, uint32_t nbuf);
 uint32_t finish_max_elems(uint32_t eb, uint32_t k);
+uint32_t finish_stream_smem_bytes(uint32_t S, uint32_t eb, uint32_t k);
+cudaError_t configure_finish_stream(uint32_t eb, uint32_t smem);
+cudaError_t launch_finish_stream(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 uint32_t finish_smem_budget(uint32_t eb);
 cudaError_t launch_finish_fast(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 cudaError_t launch_finish_fast_ip(const RunParams& rp, const IpParams& ip, cudaStream_t s, int grid);

@@ -292,3 +292,17 @@ def test_depth_overflow_is_reported():
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SHUF_LEVELS="1"), capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "err 5" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,k,L,seed,eb", [(4_000_037, 256, 2048, 41, 8), (3_900_001, 256, 2048, 42, 8),
+                                           (5_000_011, 256, 4096, 43, 4)])
+def test_stream_finish_bit_exact(n, k, L, seed, eb, monkeypatch):
+    """Children between the fused size and the single-buffer size (config-3 shape: ~15 K u64 children)
+    finish in k_finish_stream, reading the level's output straight into shared memory; with
+    SHUF_STREAM=0 they take another HBM level instead -- both equal the oracle."""
+    rng = np.random.default_rng(seed)
+    a = np.arange(n, dtype=np.uint32) if eb == 4 else rng.integers(0, 2**63, size=n, dtype=np.uint64)
+    exp = oracle.shuffle(a, k, L, seed)
+    assert (gpu_shuffle(a, k, L, seed) == exp).all()
+    monkeypatch.setenv("SHUF_STREAM", "0")
+    assert (gpu_shuffle(a, k, L, seed) == exp).all()
