@@ -50,7 +50,7 @@ namespace shuf {
 // tile, NW * k entries) cost more than the extra warps hide.
 template <int EB, bool NARROW>
 struct SCfg {
-    static constexpr uint32_t T = kScatterTileBytes / EB;  // elements per tile
+    static constexpr uint32_t T = scatter_tile_bytes(EB) / EB;  // elements per tile
     static constexpr uint32_t NW = 8;
     static constexpr uint32_t NT = NW * 32u;
     static constexpr uint32_t R = T / (NW * 32u);     // rounds per warp

@@ -308,7 +308,7 @@ extern "C" shuf_plan_t shuf_plan(uint64_t n, uint32_t elem_bytes, uint32_t k, ui
     p->seed = seed;
     p->S_fuse = S;
     p->fin_nbuf = nbuf;
-    const uint32_t T = kScatterTileBytes / elem_bytes;  // scatter tile (kernels_scatter.cu SCfg)
+    const uint32_t T = scatter_tile_bytes(elem_bytes) / elem_bytes;  // scatter tile (kernels_scatter.cu SCfg)
     // chunks per level: at most 4096 (balanced over the persistent grid), and
     // few enough that a level's count + prefix tables (12 B per (bucket,
     // chunk)) stay within ~0.5 % of the data each

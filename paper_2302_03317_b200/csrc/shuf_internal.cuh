@@ -18,6 +18,17 @@ constexpr uint32_t kSmemLimit = 227 * 1024;
 constexpr uint32_t kFinishBucketGroup = 16; // children per finish work unit
 constexpr uint32_t kMaxLevels = 256;
 constexpr uint32_t kScatterTileBytes = 32768; // HBM scatter tile (kernels_scatter.cu); chunks are multiples of it
+#ifndef SHUF_TILE16
+#define SHUF_TILE16 65536
+#endif
+#ifndef SHUF_TILE8
+#define SHUF_TILE8 32768
+#endif
+// Tile bytes per element size: 16-byte records take 64 KiB tiles (4096 records: with k = 1024,
+// config 4, 32 KiB tiles leave ~2 records per bucket run; scatter 138.8 -> 126.0 ms, r04h).
+__host__ __device__ constexpr uint32_t scatter_tile_bytes(uint32_t eb) {
+    return eb == 16 ? SHUF_TILE16 : eb == 8 ? SHUF_TILE8 : kScatterTileBytes;
+}
 constexpr uint32_t kFrontierCap = 256;      // pending in-smem sub-segments per level
 constexpr uint32_t kIpBlockBytes = 128;     // in-place mode block (kernels_inplace.cu)
 constexpr uint32_t kIpBatchCap = 2048;      // in-place mode: stripes (and segments) per batch
