@@ -12,6 +12,7 @@
 // the stable in-tile rank gives every element's destination.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include "block_ops.cuh"
 #include "shuf_internal.cuh"
 
@@ -117,8 +118,21 @@ __global__ void k_shard_counts(RunParams rp, LevelParams lp, uint64_t* __restric
 // Regenerates the draws from Philox counters; reads no element data.
 // (Replicating the counters per lane to avoid bank conflicts was measured
 // slower: 1.18 vs 1.06 ms on HOT -- the kernel is ALU-bound on Philox.)
-uint32_t hist_smem_bytes(uint32_t k) { return k * 4u; }
+// LANES (k <= 256): every lane counts into its own column of the table,
+// hist[b*32 + lane] -- the 32 atomics of one warp instruction hit 32 distinct
+// banks (random buckets into one k-entry table conflict ~3.5-way); the
+// columns are summed per bucket at the end of the chunk (rotated so a warp's
+// 32 threads read 32 distinct banks).  SHUF_HIST_LANES=0 keeps one k-entry table.
+static bool hist_lanes(uint32_t k) {
+    static const int on = [] {
+        const char* e = std::getenv("SHUF_HIST_LANES");
+        return e ? std::atoi(e) : 1;
+    }();
+    return on != 0 && k <= 256;
+}
+uint32_t hist_smem_bytes(uint32_t k) { return hist_lanes(k) ? k * 32u * 4u : k * 4u; }
 
+template <bool LANES>
 __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp) {
     extern __shared__ uint32_t hist[];
     const uint32_t nchunk = lp.ctr->nchunk;
@@ -133,11 +147,13 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
         // run while the previous level's kernels still read that slot)
     }
     const uint32_t k = rp.k;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t col = LANES ? lane : 0u, cs = LANES ? 5u : 0u;  // counter of bucket b: hist[(b << cs) | col]
     const BucketParams bp = rp.bp;
     const uint32_t sh = bp.narrow ? 4u : 3u, dpg = 1u << sh;
+    for (uint32_t b = threadIdx.x; b < (k << cs); b += kThreads) hist[b] = 0;
+    __syncthreads();
     for (uint32_t j = blockIdx.x; j < nchunk; j += gridDim.x) {
-        for (uint32_t b = threadIdx.x; b < k; b += kThreads) hist[b] = 0;
-        __syncthreads();
         const ChunkDesc ch = lp.chunks[j];
         const SegDesc sg = lp.segs[ch.seg];
         const uint64_t q0 = sg.start + (uint64_t)ch.c * rp.chunk;
@@ -158,22 +174,37 @@ __global__ void __launch_bounds__(kThreads) k_hist(RunParams rp, LevelParams lp)
                                             (w.z >> bp.shift) & msk, (w.w >> bp.shift) & msk};
 #pragma unroll
                     for (uint32_t jj = 0; jj < 16; ++jj)
-                        atomicAdd(&hist[__byte_perm(pw[jj >> 2], 0u, 0x4440u | (jj & 3u))], 1u);
+                        atomicAdd(&hist[(__byte_perm(pw[jj >> 2], 0u, 0x4440u | (jj & 3u)) << cs) | col], 1u);
                 } else {
 #pragma unroll
                     for (uint32_t jj = 0; jj < 8; ++jj)
-                        atomicAdd(&hist[bucket_from_group(w, jj, key, lp.level, pb + jj, bp)], 1u);
+                        atomicAdd(&hist[(bucket_from_group(w, jj, key, lp.level, pb + jj, bp) << cs) | col], 1u);
                 }
             } else {
                 for (uint32_t jj = 0; jj < dpg; ++jj) {
                     const uint64_t p = pb + jj;
-                    if (p >= P0 && p < P1) atomicAdd(&hist[bucket_from_group(w, jj, key, lp.level, p, bp)], 1u);
+                    if (p >= P0 && p < P1)
+                        atomicAdd(&hist[(bucket_from_group(w, jj, key, lp.level, p, bp) << cs) | col], 1u);
                 }
             }
         }
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < k; b += kThreads)
-            lp.counts[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] = hist[b];
+        for (uint32_t b = threadIdx.x; b < k; b += kThreads) {
+            uint32_t c;
+            if (LANES) {  // sum bucket b's 32 columns and clear them for the next chunk
+                c = 0;
+#pragma unroll 8
+                for (uint32_t i = 0; i < 32; ++i) {
+                    const uint32_t x = (b << 5) | ((i + b) & 31u);
+                    c += hist[x];
+                    hist[x] = 0;
+                }
+            } else {
+                c = hist[b];
+                hist[b] = 0;
+            }
+            lp.counts[sg.cbase + (uint64_t)b * sg.nchunks + ch.c] = c;
+        }
         __syncthreads();
     }
 }
@@ -358,7 +389,8 @@ cudaError_t launch_shard_counts(const RunParams& rp, const LevelParams& lp, uint
 }
 
 cudaError_t launch_hist(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
-    k_hist<<<grid, kThreads, hist_smem_bytes(rp.k), s>>>(rp, lp);
+    if (hist_lanes(rp.k)) k_hist<true><<<grid, kThreads, hist_smem_bytes(rp.k), s>>>(rp, lp);
+    else k_hist<false><<<grid, kThreads, hist_smem_bytes(rp.k), s>>>(rp, lp);
     return cudaGetLastError();
 }
 
@@ -374,8 +406,12 @@ cudaError_t launch_plan(const RunParams& rp, const LevelParams& lp, cudaStream_t
 
 cudaError_t occupancy_level(uint32_t eb, uint32_t k, int* hist, int* scan, int* scatter) {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(hist, k_hist, kThreads, hist_smem_bytes(k)))) return e;
+    if ((e = cudaFuncSetAttribute(k_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit))) return e;
+    if ((e = cudaFuncSetAttribute(k_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(hist, hist_lanes(k) ? (const void*)k_hist<true>
+                                                                               : (const void*)k_hist<false>,
+                                                           kThreads, hist_smem_bytes(k))))
+        return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(scan, k_scan, kThreads, 0))) return e;
     return occupancy_scatter(eb, k, scatter);
 }

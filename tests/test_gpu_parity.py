@@ -219,9 +219,10 @@ _ENV_CASES = (
 
 @pytest.mark.parametrize("env", [{"SHUF_FAST_FINISH": "0"}, {"SHUF_FAST_FINISH": "0", "SHUF_RANK_MODE": "match"},
                                  {"SHUF_LEAF": "0"}, {"SHUF_DEFER": "1", "SHUF_FAST_FINISH": "0"},
-                                 {"SHUF_DEFER": "1", "SHUF_FAST_FINISH": "0", "SHUF_RANK_MODE": "match"}],
+                                 {"SHUF_DEFER": "1", "SHUF_FAST_FINISH": "0", "SHUF_RANK_MODE": "match"},
+                                 {"SHUF_HIST_LANES": "0"}],
                          ids=["general_finish", "general_finish_match", "no_leaf_kernel", "deferred_leaves",
-                              "deferred_leaves_match"])
+                              "deferred_leaves_match", "hist_one_table"])
 def test_alternate_routes_bit_exact(env):
     """Routes chosen per process by environment (the general finish kernel
     instead of kernels_fast.cu's pipelined one; leaves in the finish kernel
