@@ -15,6 +15,8 @@
 // each other's latency.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "block_ops.cuh"
 #include "shuf_internal.cuh"
 
@@ -39,8 +41,10 @@ __host__ __device__ inline uint32_t leaf_slot_bytes(uint32_t eb, uint32_t L) {
 // lane l conflicts if another lane shares its partner (every lane writes its
 // id to M[j], then reads it back: a different id means a shared partner;
 // flagging both lanes of a pair is conservative, hence still exact) or if an
-// earlier lane's partner is l's own position i_l (an earlier lane's i can
-// never be l's partner, as j_l <= i_l).
+// earlier lane's partner is l's own position i_l (that lane sets bit l of
+// a warp OR-reduction; an earlier lane's i can never be l's partner, as
+// j_l <= i_l).  Lane 0's step is always safe alone, so every
+// round makes progress.
 template <int EB>
 __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, unsigned char* M, uint32_t m, uint64_t q,
                                              PhiloxKey key) {
@@ -48,6 +52,15 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
     const uint32_t lane = threadIdx.x & 31u;
     if (m < 2) return;
     const uint32_t ng = ((m - 1) >> 3) + 1;
+    // Steps whose multiply-shift candidate may be rejected (low half < s:
+    // probability s/2^16, a few % on long leaves) go to a list in M and are
+    // settled afterwards by all lanes at once (exact test: 2^16 mod s, retry
+    // stream) -- inline, the rare lane's modulo and retry held the whole warp.
+    uint32_t* ncand = reinterpret_cast<uint32_t*>(M);
+    uint32_t* cand = ncand + 4;
+    const uint32_t cap = (m >> 2) - 4;  // M holds >= m bytes; long leaves only (m > 512)
+    if (lane == 0) *ncand = 0;
+    __syncwarp();
     for (uint32_t g = lane; g < ng; g += 32) {
         const uint4 w = fy16_group_words(key, q, g);
         const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
@@ -57,11 +70,20 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
             if (i >= 1 && i < m) {
                 const uint32_t v = (wv[jj >> 1] >> ((jj & 1u) * 16u)) & 0xFFFFu;
                 const uint32_t sb = i + 1, mm = v * sb;
-                uint32_t j = mm >> 16;
-                if (__builtin_expect((mm & 0xFFFFu) < sb, 0)) j = fy16_from_lane(v, key, q, i);
-                P[i] = (uint16_t)j;
+                P[i] = (uint16_t)(mm >> 16);
+                if (__builtin_expect((mm & 0xFFFFu) < sb, 0)) {
+                    const uint32_t x = atomicAdd(ncand, 1u);
+                    if (x < cap) cand[x] = i | (v << 16);
+                    else P[i] = (uint16_t)fy16_from_lane(v, key, q, i);
+                }
             }
         }
+    }
+    __syncwarp();
+    const uint32_t nc = min(*ncand, cap);
+    for (uint32_t x = lane; x < nc; x += 32) {
+        const uint32_t e = cand[x], i = e & 0xFFFFu;
+        P[i] = (uint16_t)fy16_from_lane(e >> 16, key, q, i);
     }
     __syncwarp();
     E* A = reinterpret_cast<E*>(el);
@@ -70,17 +92,20 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
         const int32_t i = top - (int32_t)lane;
         const bool valid = i >= 1;
         const uint32_t j = valid ? (uint32_t)P[i] : 0u;
+        // both operands load before the conflict test (off the round's critical
+        // path); only the lanes that run use them, and no running lane's
+        // positions are touched by another running lane this round
+        const E a = A[valid ? i : 0], b = A[j];
         if (valid) M[j] = (unsigned char)lane;
         __syncwarp();
         const bool shared = valid && M[j] != lane;
         const int32_t d = top - (int32_t)j;  // the lane whose position is my partner
         const uint32_t hb = (valid && d < 32 && d > (int32_t)lane) ? (1u << d) : 0u;
         const uint32_t hits = __reduce_or_sync(0xFFFFFFFFu, hb);
-        const bool conflict = valid && (shared || ((hits >> lane) & 1u));
+        const bool conflict = valid && lane != 0 && (shared || ((hits >> lane) & 1u));  // lane 0 always runs
         const uint32_t cmask = __ballot_sync(0xFFFFFFFFu, conflict);
         const uint32_t c = cmask ? (uint32_t)(__ffs(cmask) - 1) : min(32u, (uint32_t)top);
         if (lane < c) {
-            const E a = A[i], b = A[j];
             A[i] = b;
             A[j] = a;
         }
@@ -88,12 +113,30 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
         top -= (int32_t)c;
     }
 }
-// Warps per leaf CTA: 4, or fewer when 4 slots exceed the shared memory
-// (e.g. 16-byte elements with L = 4096: a 64 KiB slot per warp).
+// Warps per leaf CTA (1..4): the count that puts the most warps on an SM
+// (228 KiB of shared memory, 1 KiB reserved per CTA), the larger CTA on a
+// tie.  E.g. u32 with L = 4096 (28.7 KiB slots): 4-warp CTAs fit once per SM
+// (4 warps), 1-warp CTAs 7 times (7 warps); 16-byte elements with L = 4096
+// (a 64 KiB slot) get 1-warp CTAs, 3 per SM.  SHUF_LEAF_WARPS=w forces w.
 uint32_t leaf_warps(uint32_t eb, uint32_t L) {
-    uint32_t w = kLeafWarps;
-    while (w > 1 && w * (leaf_slot_bytes(eb, L) + 16) > kSmemLimit) --w;
-    return w;
+    static const int forced = [] {
+        const char* e = std::getenv("SHUF_LEAF_WARPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    const uint32_t per = leaf_slot_bytes(eb, L) + 16;
+    if (forced >= 1 && forced <= (int)kLeafWarps && forced * per <= kSmemLimit) return (uint32_t)forced;
+    constexpr uint32_t kSmSmem = 228u * 1024u, kCtaReserve = 1024u;
+    uint32_t best = 1, best_warps = 0;
+    for (uint32_t w = 1; w <= kLeafWarps; ++w) {
+        if (w * per > kSmemLimit) break;
+        uint32_t ctas = kSmSmem / (w * per + kCtaReserve);
+        if (ctas > 32u) ctas = 32u;
+        if (ctas * w >= best_warps) {
+            best_warps = ctas * w;
+            best = w;
+        }
+    }
+    return best;
 }
 uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L) { return leaf_warps(eb, L) * (leaf_slot_bytes(eb, L) + 16); }
 
