@@ -39,8 +39,9 @@ __host__ __device__ inline uint32_t leaf_slot_bytes(uint32_t eb, uint32_t L) {
 // in rounds the lanes take steps i = top, top-1, .., top-31 and the longest
 // prefix of them that touches pairwise distinct positions runs at once --
 // lane l conflicts if another lane shares its partner (every lane writes its
-// id to M[j], then reads it back: a different id means a shared partner;
-// flagging both lanes of a pair is conservative, hence still exact) or if an
+// id to M[j], then reads it back: a different id means a shared partner --
+// of two lanes sharing one, at least the loser of the store is flagged, and
+// the prefix ends before it; lane 0's partner is also compared directly) or if an
 // earlier lane's partner is l's own position i_l (that lane sets bit l of
 // a warp OR-reduction; an earlier lane's i can never be l's partner, as
 // j_l <= i_l).  Lane 0's step is always safe alone, so every
@@ -98,7 +99,11 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
         const E a = A[valid ? i : 0], b = A[j];
         if (valid) M[j] = (unsigned char)lane;
         __syncwarp();
-        const bool shared = valid && M[j] != lane;
+        // the lane whose store to a shared M[j] survives is unspecified, so lane 0
+        // (which always runs) is compared directly: a later lane with lane 0's
+        // partner waits whichever of the two stores won
+        const uint32_t j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
+        const bool shared = valid && (M[j] != lane || (lane != 0 && j == j0));
         const int32_t d = top - (int32_t)j;  // the lane whose position is my partner
         const uint32_t hb = (valid && d < 32 && d > (int32_t)lane) ? (1u << d) : 0u;
         const uint32_t hits = __reduce_or_sync(0xFFFFFFFFu, hb);
