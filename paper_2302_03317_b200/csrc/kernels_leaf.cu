@@ -40,8 +40,8 @@ __host__ __device__ inline uint32_t leaf_slot_bytes(uint32_t eb, uint32_t L) {
 // prefix of them that touches pairwise distinct positions runs at once --
 // lane l conflicts if another lane shares its partner (every lane writes its
 // id to M[j], then reads it back: a different id means a shared partner --
-// of two lanes sharing one, at least the loser of the store is flagged, and
-// the prefix ends before it; lane 0's partner is also compared directly) or if an
+// of lanes sharing one, every loser of the store is flagged, and the prefix
+// ends before the first flagged lane, at least one step) or if an
 // earlier lane's partner is l's own position i_l (that lane sets bit l of
 // a warp OR-reduction; an earlier lane's i can never be l's partner, as
 // j_l <= i_l).  Lane 0's step is always safe alone, so every
@@ -89,6 +89,7 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
     __syncwarp();
     E* A = reinterpret_cast<E*>(el);
     int32_t top = (int32_t)m - 1;
+    const uint32_t Ms = smem_u32(M);
     while (top >= 1) {
         const int32_t i = top - (int32_t)lane;
         const bool valid = i >= 1;
@@ -97,19 +98,21 @@ __device__ __forceinline__ void fy_leaf_warp(unsigned char* el, uint16_t* P, uns
         // path); only the lanes that run use them, and no running lane's
         // positions are touched by another running lane this round
         const E a = A[valid ? i : 0], b = A[j];
-        if (valid) M[j] = (unsigned char)lane;
+        // every lane marks its own position, then its partner: a lane whose own
+        // mark was overwritten is the partner of an earlier lane; a lane whose
+        // partner mark was overwritten shares its partner
+        if (valid) sts_u8(Ms + (uint32_t)i, lane);
         __syncwarp();
-        // the lane whose store to a shared M[j] survives is unspecified, so lane 0
-        // (which always runs) is compared directly: a later lane with lane 0's
-        // partner waits whichever of the two stores won
-        const uint32_t j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
-        const bool shared = valid && (M[j] != lane || (lane != 0 && j == j0));
-        const int32_t d = top - (int32_t)j;  // the lane whose position is my partner
-        const uint32_t hb = (valid && d < 32 && d > (int32_t)lane) ? (1u << d) : 0u;
-        const uint32_t hits = __reduce_or_sync(0xFFFFFFFFu, hb);
-        const bool conflict = valid && lane != 0 && (shared || ((hits >> lane) & 1u));  // lane 0 always runs
+        if (valid) sts_u8(Ms + j, lane);
+        __syncwarp();
+        const uint32_t mj = lds_u8(Ms + j), mi = lds_u8(Ms + (valid ? (uint32_t)i : 0u));  // both loads in flight
+        const bool conflict = valid & ((mj != lane) | (mi != lane));
         const uint32_t cmask = __ballot_sync(0xFFFFFFFFu, conflict);
-        const uint32_t c = cmask ? (uint32_t)(__ffs(cmask) - 1) : min(32u, (uint32_t)top);
+        // Which of two same-address stores to M survives is unspecified: of lanes
+        // sharing a partner at least every loser is flagged, so the prefix ends
+        // before the first of them; if that is lane 0 it runs alone (a single step
+        // is always safe), which also guarantees progress.
+        const uint32_t c = cmask ? max((uint32_t)(__ffs(cmask) - 1), 1u) : min(32u, (uint32_t)top);
         if (lane < c) {
             A[i] = b;
             A[j] = a;
