@@ -147,6 +147,14 @@ uint32_t leaf_warps(uint32_t eb, uint32_t L) {
     return best;
 }
 uint32_t leaf_smem_bytes(uint32_t eb, uint32_t L) { return leaf_warps(eb, L) * (leaf_slot_bytes(eb, L) + 16); }
+uint32_t leaf_warps_per_cta(uint32_t eb, uint32_t L) { return leaf_warps(eb, L); }
+// Leaf warps resident on an SM with slots for leaves of L elements.
+uint32_t leaf_warps_per_sm(uint32_t eb, uint32_t L) {
+    const uint32_t w = leaf_warps(eb, L);
+    uint32_t ctas = (228u * 1024u) / (w * (leaf_slot_bytes(eb, L) + 16) + 1024u);
+    if (ctas > 32u) ctas = 32u;
+    return ctas * w;
+}
 
 struct Leaf {
     uint64_t start, len, origin, key;
@@ -277,7 +285,7 @@ struct IpscLeaves {
 
 template <int EB, class Src>
 __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned char* src, const Src& ls,
-                                           uint32_t slot_bytes) {
+                                           uint32_t slot_bytes, uint32_t len_lo = 0u, uint32_t len_hi = 0xFFFFFFFFu) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     unsigned char* slot = lsm + warp * (slot_bytes + 16);
     uint64_t* bar = reinterpret_cast<uint64_t*>(slot + slot_bytes);
@@ -294,8 +302,9 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
     for (uint64_t u = (uint64_t)blockIdx.x * nw + warp; u < units; u += (uint64_t)gridDim.x * nw) {
         const Leaf lf = ls.get(u, lane);
         const uint64_t start = lf.start, len = lf.len, origin = lf.origin, key = lf.key;
-        const bool fy = len >= 2 && len <= rp.L && rp.run_leaves;
-        const bool mine = len >= 1 && len <= rp.L && (fy || copy_out);
+        const bool pass = len > len_lo && len <= len_hi;  // this launch's length class
+        const bool fy = len >= 2 && len <= rp.L && rp.run_leaves && pass;
+        const bool mine = len >= 1 && len <= rp.L && (fy || copy_out) && pass;
         if (mine) fin += len;
         // long leaves (fewer than 8 fit the slot) run one at a time with the
         // whole warp (fy_leaf_warp); the others one thread per leaf
@@ -406,14 +415,15 @@ template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_children(RunParams rp, LevelParams lp) {
     const uint32_t U = lp.leaf_unit;
     const ChildLeaves ls{&lp, rp.k, (rp.k + U - 1) / U, U};
-    run_leaves<EB>(rp, lp.dst, ls, leaf_slot_bytes(EB, rp.L));
+    const uint32_t hi = lp.leaf_hi ? lp.leaf_hi : rp.L;
+    run_leaves<EB>(rp, lp.dst, ls, leaf_slot_bytes(EB, hi), lp.leaf_lo, hi);
 }
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_segments(RunParams rp, const uint64_t* __restrict__ off,
-                                                                 uint64_t nsegs, uint32_t U) {
+                                                                 uint64_t nsegs, uint32_t U, uint32_t lo, uint32_t hi) {
     const SegLeaves ls{off, nsegs, rp.seed, U, rp.shard, rp.seg_base};
-    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, rp.L));
+    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, hi), lo, hi);  // segments with lo < length <= hi
 }
 
 template <int EB>
@@ -464,16 +474,20 @@ cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks) {
 
 cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid) {
     void* args[] = {(void*)&rp, (void*)&lp};
-    return cudaLaunchKernel(leaf_fn(rp.eb, 0), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L),
-                            s);
+    const uint32_t hi = lp.leaf_hi ? lp.leaf_hi : rp.L;  // the slots hold leaves of hi elements
+    return cudaLaunchKernel(leaf_fn(rp.eb, 0), dim3(grid), dim3(32 * leaf_warps(rp.eb, hi)), args,
+                            leaf_smem_bytes(rp.eb, hi), s);
 }
 
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
-                                 cudaStream_t s, int grid) {
-    uint32_t U = leaf_unit(rp.eb, rp.L, num_segments ? rp.n / num_segments : 0);
-    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments, (void*)&U};
-    return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(32 * leaf_warps(rp.eb, rp.L)), args, leaf_smem_bytes(rp.eb, rp.L),
-                            s);
+                                 cudaStream_t s, int grid, uint32_t lo, uint32_t hi) {
+    if (hi == 0) hi = rp.L;  // the slots hold segments of hi elements
+    uint64_t avg = num_segments ? rp.n / num_segments : 0;
+    if (avg > hi) avg = hi;
+    uint32_t U = leaf_unit(rp.eb, hi, avg);
+    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments, (void*)&U, (void*)&lo, (void*)&hi};
+    return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(32 * leaf_warps(rp.eb, hi)), args,
+                            leaf_smem_bytes(rp.eb, hi), s);
 }
 
 cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid) {

@@ -41,6 +41,7 @@ struct shuf_plan_s {
     int grid_hist, grid_scan, grid_scatter, grid_finish, grid_small, grid_fast, grid_leaf;
     int fast, leafk, defer;
     int hist_overlap;             // 1: level l+1's histogram runs on side_stream during level l's scatter
+    double leaf_sigma;            // small-slot leaf pass: slots hold avg + leaf_sigma * sqrt(avg) elements (< 0: off)
     cudaStream_t side_stream;
     cudaEvent_t ev_fork, ev_join;
     bool ip_ready;
@@ -444,6 +445,10 @@ static cudaError_t device_setup(shuf_plan_s* p) {
     // the next level's histogram (reads no data: positions only) on a side
     // stream, overlapping the current level's scatter (SHUF_HIST_OVERLAP=1; off by
     // default: the scatter holds every register of the SM, so the two do not co-run)
+    {  // SHUF_LEAF_SIGMA: 12 by default; 0 sends about half of the leaves to the second pass (tests); -1 = one pass
+        const char* ls = std::getenv("SHUF_LEAF_SIGMA");
+        p->leaf_sigma = ls ? std::atof(ls) : 12.0;
+    }
     {
         const char* ho = std::getenv("SHUF_HIST_OVERLAP");
         p->hist_overlap = (ho && ho[0] == '1') ? 1 : 0;  // measured: no gain
@@ -505,6 +510,7 @@ static LevelParams level_params(const ScratchLayout& l, unsigned char* sc, unsig
     lp.src = (level & 1u) ? buf1 : buf0;
     lp.dst = (level & 1u) ? buf0 : buf1;
     lp.leaf_unit = 32;
+    lp.leaf_lo = lp.leaf_hi = 0;
     return lp;
 }
 
@@ -668,6 +674,17 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
             double avg = (double)rp.n / (double)(d_offsets ? (nsegs ? nsegs : 1) : 1);
             for (uint32_t i = 0; i <= lv; ++i) avg /= (double)p->k;
             lp.leaf_unit = leaf_unit(p->eb, p->L, (uint64_t)avg);
+            // Single shuffle, long leaves (one per warp) expected well below L: a
+            // first leaf pass whose slots hold avg + leaf_sigma * sqrt(avg) elements
+            // (child lengths are binomial: sigma < sqrt(avg)) when that puts more
+            // warps on an SM, then the full-slot pass for longer leaves (normally none).
+            if (!d_offsets && p->leaf_sigma >= 0.0 && avg <= (double)p->L && lp.leaf_unit == 1) {
+                uint64_t cand = (uint64_t)(avg + p->leaf_sigma * std::sqrt(avg)) + 1;
+                cand = (cand + 63) & ~63ull;
+                if (cand < p->L && leaf_unit(p->eb, (uint32_t)cand, (uint64_t)avg) == 1 &&
+                    leaf_warps_per_sm(p->eb, (uint32_t)cand) > leaf_warps_per_sm(p->eb, p->L))
+                    lp.leaf_hi = (uint32_t)cand;
+            }
         }
         if (overlap && lv > 0) {
             if ((e = cudaStreamWaitEvent(st, p->ev_join, 0))) return cuda_fail(p, e);
@@ -688,7 +705,18 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
         if (p->fast) LAUNCH(SHUF_K_FINISH, launch_finish_fast(rp, lp, st, p->grid_fast));
         LAUNCH(SHUF_K_FINISH, launch_finish_children(rp, lp, st, p->grid_finish));
         if (p->S_stream) LAUNCH(SHUF_K_FINISH, launch_finish_stream(rp, lp, st, p->sms));
-        if (p->leafk) LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->grid_leaf));
+        if (p->leafk) {
+            if (lp.leaf_hi) {
+                const uint32_t wps = leaf_warps_per_sm(p->eb, lp.leaf_hi), wpc = leaf_warps_per_cta(p->eb, lp.leaf_hi);
+                LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->sms * (int)(wps / wpc)));
+                LevelParams rest = lp;
+                rest.leaf_lo = lp.leaf_hi;
+                rest.leaf_hi = 0;
+                LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, rest, st, p->grid_leaf));
+            } else {
+                LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->grid_leaf));
+            }
+        }
         if (lv + lv0 + 1 == max_levels) LAUNCH(SHUF_K_FINISH, launch_copy_big(rp, lp, st, p->grid_small));
     }
     // leaves of the recorded fused items (all levels; they sit in ptr)

@@ -157,6 +157,11 @@ struct LevelParams {
     unsigned char* src;  // level input buffer
     unsigned char* dst;  // level output buffer
     uint32_t leaf_unit;  // leaves per warp-unit of k_leaf_children (1 or 32, leaf_unit())
+    // k_leaf_children takes the leaves with leaf_lo < length <= leaf_hi; its warp
+    // slots hold a leaf of leaf_hi elements (leaf_hi = 0: L).  A level whose
+    // expected leaf length is well below L runs a first pass with small slots
+    // (more warps per SM) and a second pass with full slots for the outliers.
+    uint32_t leaf_lo, leaf_hi;
 };
 
 // ------------------------------------------------------- in-place mode ---
@@ -293,9 +298,12 @@ cudaError_t launch_finish_fast_ip(const RunParams& rp, const IpParams& ip, cudaS
 cudaError_t configure_fast(uint32_t eb, uint32_t k);
 uint32_t fast_smem_bytes(uint32_t eb, uint32_t k);
 uint32_t leaf_unit(uint32_t eb, uint32_t L, uint64_t avg);
+uint32_t leaf_warps_per_sm(uint32_t eb, uint32_t L);
+uint32_t leaf_warps_per_cta(uint32_t eb, uint32_t L);
 cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
+// segments with lo < length <= hi (hi = 0: L), warp slots sized for hi elements
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
-                                 cudaStream_t s, int grid);
+                                 cudaStream_t s, int grid, uint32_t lo = 0, uint32_t hi = 0);
 cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid);
 cudaError_t configure_leaf(uint32_t eb, uint32_t L);
 cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks);

@@ -307,3 +307,32 @@ def test_stream_finish_bit_exact(n, k, L, seed, eb, monkeypatch):
     assert (gpu_shuffle(a, k, L, seed) == exp).all()
     monkeypatch.setenv("SHUF_STREAM", "0")
     assert (gpu_shuffle(a, k, L, seed) == exp).all()
+
+
+@pytest.mark.parametrize("n,k,L,seed", [(4_200_003, 64, 4096, 51), (600_001, 16, 4096, 52), (9_000_017, 64, 4096, 53)])
+def test_leaf_two_pass_slots_bit_exact(n, k, L, seed, monkeypatch):
+    """Long leaves expected well below L (config-2 shape: ~L/2) run a first leaf pass with small
+    slots and a second pass with full slots for the longer ones.  SHUF_LEAF_SIGMA=0 puts the
+    cut at the expected length (about half of the leaves in each pass), -1 is the single pass;
+    all equal the oracle (Fig. 1 leaves)."""
+    a = np.arange(n, dtype=np.uint32)
+    exp = oracle.shuffle(a, k, L, seed)
+    assert (gpu_shuffle(a, k, L, seed) == exp).all()
+    for sigma in ("0", "-1", "3"):
+        monkeypatch.setenv("SHUF_LEAF_SIGMA", sigma)
+        assert (gpu_shuffle(a, k, L, seed) == exp).all(), sigma
+
+
+def test_segmented_long_leaves_bit_exact(monkeypatch):
+    """Segmented mode with thousands of long segments (one per warp in the leaf kernel): lengths
+    across (0, L], the values around L/2, 3L/4 and L, 0, 1 and L + 1 (D7); SHUF_LEAF_SIGMA=-1
+    (no small-slot leaf pass anywhere) gives the same bits."""
+    rng = np.random.default_rng(77)
+    lens = rng.integers(300, 4097, size=3000).astype(np.int64)
+    lens[:12] = [0, 1, 2, 2047, 2048, 2049, 3071, 3072, 3073, 4095, 4096, 4097]
+    off = synth.segment_offsets(lens)
+    a = np.arange(int(off[-1]), dtype=np.uint32)
+    exp = oracle.segmented(a, off, 64, 4096, 9)
+    assert (gpu_segmented(a, off, 64, 4096, 9) == exp).all()
+    monkeypatch.setenv("SHUF_LEAF_SIGMA", "-1")
+    assert (gpu_segmented(a, off, 64, 4096, 9) == exp).all()
