@@ -285,7 +285,8 @@ struct IpscLeaves {
 
 template <int EB, class Src>
 __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned char* src, const Src& ls,
-                                           uint32_t slot_bytes, uint32_t len_lo = 0u, uint32_t len_hi = 0xFFFFFFFFu) {
+                                           uint32_t slot_bytes, uint32_t len_lo = 0u, uint32_t len_hi = 0xFFFFFFFFu,
+                                           unsigned long long* ticket = nullptr) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     unsigned char* slot = lsm + warp * (slot_bytes + 16);
     uint64_t* bar = reinterpret_cast<uint64_t*>(slot + slot_bytes);
@@ -299,7 +300,14 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
     const bool copy_out = src != rp.buf0;
     unsigned long long fyn = 0, fin = 0;
     const uint32_t nw = blockDim.x >> 5;  // leaf_warps()
-    for (uint64_t u = (uint64_t)blockIdx.x * nw + warp; u < units; u += (uint64_t)gridDim.x * nw) {
+    // warp-units by a fixed stride, or (ticket != nullptr) the next one from a global counter:
+    // with leaves of very different lengths the stride leaves some warps far behind
+    unsigned long long tk = 0;
+    if (ticket && lane == 0) tk = atomicAdd(ticket, 1ull);
+    uint64_t u = ticket ? __shfl_sync(0xFFFFFFFFu, tk, 0) : (uint64_t)blockIdx.x * nw + warp;
+    for (; u < units;) {
+        if (ticket && lane == 0) tk = atomicAdd(ticket, 1ull);  // the next unit's ticket, in flight during this unit
+        const uint64_t ustep = (uint64_t)gridDim.x * nw;
         const Leaf lf = ls.get(u, lane);
         const uint64_t start = lf.start, len = lf.len, origin = lf.origin, key = lf.key;
         const bool pass = len > len_lo && len <= len_hi;  // this launch's length class
@@ -399,6 +407,7 @@ __device__ __forceinline__ void run_leaves(const RunParams& rp, const unsigned c
             }
             __syncwarp();
         }
+        u = ticket ? __shfl_sync(0xFFFFFFFFu, tk, 0) : u + ustep;
     }
     for (int o = 16; o > 0; o >>= 1) {
         fyn += __shfl_xor_sync(0xFFFFFFFFu, fyn, o);
@@ -421,9 +430,10 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_children(RunParams rp, Le
 
 template <int EB>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_segments(RunParams rp, const uint64_t* __restrict__ off,
-                                                                 uint64_t nsegs, uint32_t U, uint32_t lo, uint32_t hi) {
+                                                                 uint64_t nsegs, uint32_t U, uint32_t lo, uint32_t hi,
+                                                                 unsigned long long* ticket) {
     const SegLeaves ls{off, nsegs, rp.seed, U, rp.shard, rp.seg_base};
-    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, hi), lo, hi);  // segments with lo < length <= hi
+    run_leaves<EB>(rp, rp.buf0, ls, leaf_slot_bytes(EB, hi), lo, hi, ticket);  // segments with lo < length <= hi
 }
 
 template <int EB>
@@ -480,12 +490,13 @@ cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cud
 }
 
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
-                                 cudaStream_t s, int grid, uint32_t lo, uint32_t hi) {
+                                 cudaStream_t s, int grid, uint32_t lo, uint32_t hi, unsigned long long* ticket) {
     if (hi == 0) hi = rp.L;  // the slots hold segments of hi elements
     uint64_t avg = num_segments ? rp.n / num_segments : 0;
     if (avg > hi) avg = hi;
     uint32_t U = leaf_unit(rp.eb, hi, avg);
-    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments, (void*)&U, (void*)&lo, (void*)&hi};
+    void* args[] = {(void*)&rp, (void*)&d_offsets, (void*)&num_segments, (void*)&U, (void*)&lo, (void*)&hi,
+                    (void*)&ticket};
     return cudaLaunchKernel(leaf_fn(rp.eb, 1), dim3(grid), dim3(32 * leaf_warps(rp.eb, hi)), args,
                             leaf_smem_bytes(rp.eb, hi), s);
 }

@@ -653,7 +653,37 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
     if (d_offsets) {
         LAUNCH(SHUF_K_INIT, launch_init_segmented(rp, lp0, d_offsets, nsegs, st, p->grid_small));
         LAUNCH(SHUF_K_FINISH, launch_finish_segments(rp, d_offsets, nsegs, st, p->grid_finish));
-        if (p->leafk) LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, d_offsets, nsegs, st, p->grid_leaf));
+        if (p->leafk) {
+            // Long segments (one per warp): length classes (0, L/2], (L/2, 3L/4], (3L/4, L], each pass
+            // with slots for its class -- the shorter classes put more warps on an SM -- and warp-units
+            // handed out by a ticket counter (a fixed stride plus the class filter left warps unevenly
+            // loaded, r06i).  The host does not know the lengths; a pass that finds no segment of its
+            // class only reads offsets.  SHUF_LEAF_SIGMA=-1: one pass, fixed stride.
+            uint32_t cuts[3] = {0, 0, p->L};
+            int nc = 1;
+            const uint64_t avg = nsegs ? rp.n / nsegs : 0;
+            const bool classes = !so && p->leaf_sigma >= 0.0 && nsegs >= 1024 &&
+                                 leaf_unit(p->eb, p->L, avg > p->L ? p->L : avg) == 1;
+            if (classes) {
+                uint32_t prev = p->L;
+                for (uint32_t c : {(3 * p->L / 4 + 63) & ~63u, (p->L / 2 + 63) & ~63u}) {
+                    if (c >= 512 && c < prev && leaf_warps_per_sm(p->eb, c) > leaf_warps_per_sm(p->eb, prev)) {
+                        cuts[2 - nc] = c;
+                        ++nc;
+                        prev = c;
+                    }
+                }
+            }
+            uint32_t lo = 0;
+            for (int i = 3 - nc; i < 3; ++i) {
+                const uint32_t hi = cuts[i];
+                const int g = hi == p->L ? p->grid_leaf
+                                         : p->sms * (int)(leaf_warps_per_sm(p->eb, hi) / leaf_warps_per_cta(p->eb, hi));
+                LAUNCH(SHUF_K_LEAF, launch_leaf_segments(rp, d_offsets, nsegs, st, g, lo, hi,
+                                                         classes ? &hdr->leaf_ticket[i] : nullptr));
+                lo = hi;
+            }
+        }
     } else {
         LAUNCH(SHUF_K_INIT, launch_init(rp, lp0, st, p->grid_small));
         if (p->n <= p->S_fuse) {
@@ -712,6 +742,7 @@ static shuf_status enqueue(shuf_plan_s* p, void* ptr, const uint64_t* d_offsets,
                 LevelParams rest = lp;
                 rest.leaf_lo = lp.leaf_hi;
                 rest.leaf_hi = 0;
+                rest.leaf_unit = 32;  // normally no leaf at all: look at 32 children per warp-unit
                 LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, rest, st, p->grid_leaf));
             } else {
                 LAUNCH(SHUF_K_LEAF, launch_leaf_children(rp, lp, st, p->grid_leaf));

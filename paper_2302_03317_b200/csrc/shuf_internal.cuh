@@ -66,7 +66,10 @@ struct Header {
     LevelCounters lv[2];
     uint64_t root_off[2];  // {0, n}: the single problem as a one-segment batch
     uint32_t error;        // latched shuf_status detected on the device
-    uint32_t pad[7];
+    uint32_t pad0;
+    // work tickets of the segmented mode's leaf passes (one per pass; zeroed with the header):
+    // warps take the next warp-unit from the pass's counter instead of a fixed stride
+    unsigned long long leaf_ticket[3];
     // measurement counters (one atomic per chunk / per shared-memory scatter)
     uint64_t scattered_hbm[kMaxLevels];   // elements scattered through HBM at level l
     uint64_t scattered_smem[kMaxLevels];  // elements scattered in shared memory at level l
@@ -303,7 +306,8 @@ uint32_t leaf_warps_per_cta(uint32_t eb, uint32_t L);
 cudaError_t launch_leaf_children(const RunParams& rp, const LevelParams& lp, cudaStream_t s, int grid);
 // segments with lo < length <= hi (hi = 0: L), warp slots sized for hi elements
 cudaError_t launch_leaf_segments(const RunParams& rp, const uint64_t* d_offsets, uint64_t num_segments,
-                                 cudaStream_t s, int grid, uint32_t lo = 0, uint32_t hi = 0);
+                                 cudaStream_t s, int grid, uint32_t lo = 0, uint32_t hi = 0,
+                                 unsigned long long* ticket = nullptr);
 cudaError_t launch_leaf_items(const RunParams& rp, cudaStream_t s, int grid);
 cudaError_t configure_leaf(uint32_t eb, uint32_t L);
 cudaError_t occupancy_leaf(uint32_t eb, uint32_t L, int* blocks);
