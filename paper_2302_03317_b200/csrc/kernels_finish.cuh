@@ -655,25 +655,47 @@ __global__ void __launch_bounds__(NTF, 1) k_finish_ipchildren(RunParams rp, IpPa
 struct SegIter {
     const RunParams* rp;
     const uint64_t* off;
-    __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {  // warp 0, all lanes
+    // warp 0, all lanes: the lanes look at the CTA's next 32 segments at once (in the segmented mode
+    // most segments are the leaf kernel's; one lane walking them paid two dependent global loads each)
+    __device__ __forceinline__ void next(FinCtl* ctl, uint32_t slot) const {
         const uint32_t lane = threadIdx.x & 31u;
+        uint64_t u = ctl->u;
+        const uint64_t units = ctl->units;
+        bool found = false;
+        uint64_t si = 0, a = 0, b = 0;
+        while (u < units) {
+            const uint64_t s = u + (uint64_t)lane * gridDim.x;
+            uint64_t sa = 0, sb = 0;
+            bool ok = false;
+            if (s < units) {
+                sa = off[s];
+                sb = off[s + 1];
+                ok = sb > sa && sb - sa <= rp->S_fuse && !(rp->leafk && sb - sa <= rp->L) &&  // not the leaf kernel's
+                     item_permutes(*rp, (uint32_t)(sb - sa), rp->first_level);
+            }
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+            if (m) {
+                const int f = __ffs(m) - 1;
+                si = __shfl_sync(0xFFFFFFFFu, s, f);
+                a = __shfl_sync(0xFFFFFFFFu, sa, f);
+                b = __shfl_sync(0xFFFFFFFFu, sb, f);
+                u = si + gridDim.x;
+                found = true;
+                break;
+            }
+            u += 32ull * gridDim.x;
+        }
+        __syncwarp();  // every lane has read ctl->u
         if (lane == 0) {
-            ctl->have[slot] = 0;
-            while (ctl->u < ctl->units) {
-                const uint64_t si = ctl->u;
-                ctl->u += gridDim.x;
-                const uint64_t a = off[si], b = off[si + 1];
-                if (b <= a || b - a > rp->S_fuse) continue;
-                if (rp->leafk && b - a <= rp->L) continue;  // the leaf kernel's
-                if (!item_permutes(*rp, (uint32_t)(b - a), rp->first_level)) continue;
+            ctl->u = u;
+            ctl->have[slot] = found ? 1u : 0u;
+            if (found) {
                 Item& it = ctl->items[slot];
                 it.start = a;
                 it.len = (uint32_t)(b - a);
                 it.level = rp->first_level;
                 it.origin = rp->shard ? 0ull - rp->seg_base : a;
                 it.key = rp->shard ? rp->seed : rp->seed + si * 0x9E3779B97F4A7C15ull;  // K(seed, s) (D2)
-                ctl->have[slot] = 1;
-                break;
             }
         }
         __syncwarp();
